@@ -63,6 +63,8 @@ def random_scene(seed: int, W: int, H: int, D: int, alpha: float = 0.4,
     sc = Scene(W=W, H=H, D=D, alpha=alpha, horizon_row=horizon_row, **kw)
     nb = int(rng.integers(n_boxes[0], n_boxes[1] + 1))
     r_min = int(np.ceil(horizon_row)) + 2
+    if r_min >= H:          # degenerate (tiny) frames: no room for boxes
+        nb = 0
     for _ in range(nb):
         w = int(rng.integers(min(min_w, W), min(max_w, W) + 1))
         x0 = int(rng.integers(0, max(1, W - w + 1)))

@@ -1,0 +1,541 @@
+// api.cu -- host side of the C ABI declared in include/stixels.h.
+//
+// Builds the input-independent tables of the paper's LUT scheme on the host
+// ("most of the terms in the equation do not depend on the input
+// data and can be pre-computed"; the off-line D x D pair-cost LUT, here
+// in its |f - d| form since sigma is per class, L#2), validates parameters,
+// owns device memory, and launches the two sm_100a kernels of kernels.cuh.
+// There is no CPU compute path: the host only prepares tables and launches.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/stixels.h"
+#include "kernels.cuh"
+
+using namespace stx;
+
+struct stixels_handle {
+  stixels_params p{};
+  int W = 0, H = 0, max_batch = 0, device = 0;
+  cudaStream_t stream = nullptr;
+  int n_cols = 0, cap = 0, dp_slots = 128, cols_per_cta = 0, smem = 0, grid = 0, sms = 0;
+  int red_tc = 0, red_smem = 0;
+  DPArgs args{};
+  float* d_E = nullptr;
+  uint32_t* d_M2 = nullptr;
+  float* d_gG = nullptr;
+  float* d_gS = nullptr;
+  int* d_dgR = nullptr;
+  int* d_overflow = nullptr;
+  float* d_scratch = nullptr;
+  uint16_t* d_cols = nullptr;
+  // host-buffer path (lazily allocated)
+  cudaStream_t hs[2] = {nullptr, nullptr};
+  uint8_t* hin[2] = {nullptr, nullptr};
+  stixel_t* hout[2] = {nullptr, nullptr};
+  int32_t* hcnt[2] = {nullptr, nullptr};
+  float* hcost[2] = {nullptr, nullptr};
+  uint16_t* hcols[2] = {nullptr, nullptr};
+  int h_chunk = 0;
+  int64_t h_pitch = 0;
+  std::string err;
+  int sticky = 0;
+  int launches = 0;
+};
+
+static thread_local std::string g_create_err;
+
+static int fail(stixels_handle* h, int code, const std::string& msg) {
+  if (h) {
+    h->err = msg;
+    if (code == STIXELS_ERR_CUDA) h->sticky = code;
+  } else {
+    g_create_err = msg;
+  }
+  return code;
+}
+
+#define CU(call, h)                                                                         \
+  do {                                                                                      \
+    cudaError_t e_ = (call);                                                                \
+    if (e_ != cudaSuccess)                                                                  \
+      return fail(h, STIXELS_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// Model arithmetic on the host (double), written from the paper.
+// ---------------------------------------------------------------------------
+namespace {
+
+constexpr double kPi = 3.14159265358979323846;
+
+struct Host {
+  const stixels_params& p;
+  int h;
+  double R = 256.0;
+  explicit Host(const stixels_params& pp, int hh) : p(pp), h(hh) {}
+
+  // cost quantization to 2^-q nats (L#22); continuous when q == 0
+  double Q(double x) const {
+    if (std::isinf(x)) return x;
+    if (p.cost_frac_bits <= 0) return x;
+    return (double)std::llrint(std::ldexp(x, p.cost_frac_bits));
+  }
+  static double nl(double prob) { return prob <= 0.0 ? INFINITY : -std::log(prob); }
+  // Eq. 4, sigma per class, natural log (L#4, L#5, L#7)
+  double eq4(double delta, double sigma) const {
+    double unif = std::log((double)p.max_disparity) - std::log((double)p.p_out);
+    double g = std::log((double)p.a_norm) + std::log(sigma * std::sqrt(2.0 * kPi)) -
+               std::log(1.0 - (double)p.p_out) + (delta * delta) / (2.0 * sigma * sigma);
+    return g < unif ? g : unif;
+  }
+  double cap() const { return std::log((double)p.max_disparity) - std::log((double)p.p_out); }
+  double alpha() const {
+    if (p.ground_slope > 0.0f) return (double)p.ground_slope;
+    double th = std::atan(((double)p.principal_row - (double)p.horizon_row) / (double)p.focal_px);
+    return (double)p.baseline_m * std::cos(th) / (double)p.camera_height_m;
+  }
+  // ground model f_ground(v) = alpha (v_hor - v), v from the bottom, clamp >= 0,
+  // in 1/256 units rounded half up (L#12, L#14)
+  long long ground_R(int v) const {
+    double vh = (double)(h - 1) - (double)p.horizon_row;
+    double x = alpha() * (vh - (double)v);
+    if (x <= 0.0) return 0;
+    return (long long)std::floor(x * R + 0.5);
+  }
+};
+
+long long floor_div(long long a, long long b) {
+  long long q = a / b;
+  if ((a % b != 0) && ((a < 0) != (b < 0))) --q;
+  return q;
+}
+long long ceil_div(long long a, long long b) { return -floor_div(-a, b); }
+
+bool prob_ok(float x) { return std::isfinite(x) && x >= 0.f && x <= 1.f; }
+
+int validate(const stixels_params* p, int W, int H, int max_batch, std::string& msg) {
+  if (!p) { msg = "params is NULL"; return STIXELS_ERR_ARG; }
+  if (H < 1 || W < 1 || max_batch < 1) { msg = "width, height and max_batch must be >= 1"; return STIXELS_ERR_ARG; }
+  if (p->stixel_width < 1) { msg = "stixel_width must be >= 1 (S:56)"; return STIXELS_ERR_PARAM; }
+  if (W < p->stixel_width) { msg = "width < stixel_width gives no column (S:125)"; return STIXELS_ERR_ARG; }
+  if (p->stixel_width > 512) { msg = "stixel_width > 512 not supported"; return STIXELS_ERR_UNSUPPORTED; }
+  if (H > kMaxH) { msg = "height > 1024 not supported"; return STIXELS_ERR_UNSUPPORTED; }
+  if (!(p->p_out > 0.f && p->p_out < 1.f)) { msg = "need 0 < p_out < 1 (S:44)"; return STIXELS_ERR_PARAM; }
+  for (int c = 0; c < 3; ++c)
+    if (!(p->sigma[c] > 0.f) || !std::isfinite(p->sigma[c])) { msg = "sigma must be > 0"; return STIXELS_ERR_PARAM; }
+  if (!(p->a_norm > 0.f) || !std::isfinite(p->a_norm)) { msg = "a_norm must be > 0"; return STIXELS_ERR_PARAM; }
+  if (p->max_disparity < 2) { msg = "max_disparity must be >= 2 (S:44)"; return STIXELS_ERR_PARAM; }
+  if (p->max_disparity > 256) { msg = "max_disparity > 256 not supported"; return STIXELS_ERR_UNSUPPORTED; }
+  if (!std::isfinite(p->horizon_row)) { msg = "horizon_row must be finite (S:38)"; return STIXELS_ERR_PARAM; }
+  if (!(p->ground_slope > 0.f)) {
+    if (!(p->focal_px > 0.f) || !(p->camera_height_m > 0.f) || !(p->baseline_m > 0.f) ||
+        !std::isfinite(p->principal_row)) {
+      msg = "ground_slope <= 0 needs focal_px, baseline_m, camera_height_m > 0"; return STIXELS_ERR_PARAM;
+    }
+  }
+  for (int c = 0; c < 3; ++c) {
+    if (!prob_ok(p->p_first[c])) { msg = "p_first must be in [0,1]"; return STIXELS_ERR_PARAM; }
+    for (int d = 0; d < 3; ++d)
+      if (!prob_ok(p->p_trans[c][d])) { msg = "p_trans must be in [0,1]"; return STIXELS_ERR_PARAM; }
+  }
+  if (!prob_ok(p->p_ord) || !prob_ok(p->p_grav) || !prob_ok(p->p_blg) || !prob_ok(p->p_exist) ||
+      p->p_grav + p->p_blg > 1.f) {
+    msg = "p_ord, p_grav, p_blg, p_exist must be probabilities, p_grav + p_blg <= 1"; return STIXELS_ERR_PARAM;
+  }
+  if (p->p_first[STIXELS_SKY] != 0.f || p->p_trans[0][0] != 0.f || p->p_trans[2][2] != 0.f ||
+      p->p_trans[2][0] != 0.f || p->p_trans[2][1] != 0.f) {
+    msg = "structurally forbidden prior entries must be 0: p_first[sky], p_trans[G][G], "
+          "p_trans[S][S], p_trans[S][G], p_trans[S][O] (L#16)";
+    return STIXELS_ERR_PARAM;
+  }
+  if (p->ord_margin < 0 || p->grav_margin < 0 || p->ord_margin > 255 || p->grav_margin > 255) {
+    msg = "margins must be in [0, 255]"; return STIXELS_ERR_PARAM;
+  }
+  if (p->disp_format != STIXELS_U8 && p->disp_format != STIXELS_U16) { msg = "disp_format must be U8 or U16"; return STIXELS_ERR_PARAM; }
+  if (p->disp_frac_bits < 0 || p->disp_frac_bits > 8) { msg = "disp_frac_bits must be in [0, 8]"; return STIXELS_ERR_PARAM; }
+  if (p->reduce_mode != 0) { msg = "only reduce_mode 0 (mean, P:195) is implemented"; return STIXELS_ERR_UNSUPPORTED; }
+  if (p->cost_frac_bits < 0 || p->cost_frac_bits > 20) { msg = "cost_frac_bits must be in [0, 20]"; return STIXELS_ERR_PARAM; }
+  if (p->max_stixels < 0) { msg = "max_stixels must be >= 0"; return STIXELS_ERR_PARAM; }
+  return STIXELS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int stixels_default_params(stixels_params* p) {
+  if (!p) return STIXELS_ERR_ARG;
+  std::memset(p, 0, sizeof(*p));
+  p->focal_px = 1000.f; p->baseline_m = 0.3f; p->camera_height_m = 1.2f;
+  p->horizon_row = 132.f; p->principal_row = 0.f; p->ground_slope = 0.4f;
+  p->p_out = 0.15f;
+  p->sigma[0] = 2.0f; p->sigma[1] = 1.0f; p->sigma[2] = 0.5f;
+  p->a_norm = 1.0f;
+  p->p_first[0] = 1.0f; p->p_first[1] = (float)std::exp(-2.0); p->p_first[2] = 0.f;
+  for (int a = 0; a < 3; ++a) for (int b = 0; b < 3; ++b) p->p_trans[a][b] = 1.f;
+  p->p_trans[0][0] = p->p_trans[2][2] = p->p_trans[2][0] = p->p_trans[2][1] = 0.f;
+  p->p_ord = 0.2f; p->p_grav = 0.1f; p->p_blg = 0.04f; p->p_exist = (float)std::exp(-4.0);
+  p->ord_margin = 1; p->grav_margin = 1;
+  p->stixel_width = 5; p->max_disparity = 128;
+  p->disp_format = STIXELS_U16; p->disp_frac_bits = 4; p->invalid_value = 0xFFFF;
+  p->reduce_mode = 0; p->cost_frac_bits = 11; p->max_stixels = 0;
+  return STIXELS_OK;
+}
+
+const char* stixels_error_string(int s) {
+  switch (s) {
+    case STIXELS_OK: return "ok";
+    case STIXELS_ERR_ARG: return "invalid argument";
+    case STIXELS_ERR_PARAM: return "invalid parameter";
+    case STIXELS_ERR_UNSUPPORTED: return "unsupported configuration";
+    case STIXELS_ERR_CUDA: return "CUDA error";
+    case STIXELS_ERR_CAPACITY: return "per-column stixel capacity exceeded";
+    default: return "unknown status";
+  }
+}
+
+const char* stixels_last_error(const stixels_handle* h) {
+  return h ? h->err.c_str() : g_create_err.c_str();
+}
+
+static void free_all(stixels_handle* h) {
+  cudaFree(h->d_E); cudaFree(h->d_M2); cudaFree(h->d_gG); cudaFree(h->d_gS);
+  cudaFree(h->d_dgR); cudaFree(h->d_overflow); cudaFree(h->d_cols); cudaFree(h->d_scratch);
+  for (int i = 0; i < 2; ++i) {
+    cudaFree(h->hin[i]); cudaFree(h->hout[i]); cudaFree(h->hcnt[i]); cudaFree(h->hcost[i]);
+    cudaFree(h->hcols[i]);
+    if (h->hs[i]) cudaStreamDestroy(h->hs[i]);
+  }
+}
+
+int stixels_create(const stixels_params* params, int width, int height, int max_batch,
+                   int device, void* cuda_stream, stixels_handle** out) {
+  g_create_err.clear();
+  if (!out) return fail(nullptr, STIXELS_ERR_ARG, "out is NULL");
+  *out = nullptr;
+  std::string msg;
+  int st = validate(params, width, height, max_batch, msg);
+  if (st != STIXELS_OK) return fail(nullptr, st, msg);
+
+  stixels_handle* h = new stixels_handle();
+  h->p = *params;
+  h->W = width; h->H = height; h->max_batch = max_batch; h->device = device;
+  h->stream = (cudaStream_t)cuda_stream;
+  h->n_cols = width / params->stixel_width;
+  h->cap = params->max_stixels > 0 ? std::min(params->max_stixels, height) : height;
+  const int D = params->max_disparity;
+  h->dp_slots = D <= 128 ? 128 : 256;
+
+  auto bail = [&](int code, const std::string& m) {
+    g_create_err = m.empty() ? h->err : m;
+    free_all(h);
+    delete h;
+    return code;
+  };
+
+  // ---------------- host tables --------------------------------------------
+  Host hm(*params, height);
+  const double capQ = hm.Q(hm.cap());
+  const int R = 256;
+  std::vector<float> gG, gS;
+  // ground / sky cost by distance to the model disparity in 1/256 units
+  for (int i = 0;; ++i) {
+    double v = hm.Q(hm.eq4((double)i / R, (double)params->sigma[0]));
+    gG.push_back((float)v);
+    if (v >= capQ || i > D * R) break;
+  }
+  for (int i = 0;; ++i) {
+    double v = hm.Q(hm.eq4((double)i / R, (double)params->sigma[2]));
+    gS.push_back((float)v);
+    if (v >= capQ || i > D * R) break;
+  }
+  gG.back() = (float)capQ;   // clamp index -> cap (monotone Eq. 4)
+  gS.back() = (float)capQ;
+  // object pair-cost LUT Pair[f][d] = Eq4(d - f, sigma_O) as E[f - d + D]
+  const int DPv = h->dp_slots;
+  const int einv = ((D + DPv + 4) + 3) & ~3;
+  const int esz = einv + DPv + 8;
+  std::vector<float> E1((size_t)esz + 8);
+  for (int i = 0; i < esz + 8; ++i)
+    E1[i] = (i < einv) ? (float)hm.Q(hm.eq4((double)(i - D), (double)params->sigma[1])) : (float)capQ;
+  std::vector<float> E4((size_t)4 * esz);
+  for (int c = 0; c < 4; ++c)
+    for (int i = 0; i < esz; ++i) E4[(size_t)c * esz + i] = E1[i + c];
+  // magic reciprocals: floor(y/(2n)) = umulhi(y, ceil(2^31/n))
+  std::vector<uint32_t> M2(height + 1);
+  M2[0] = 0;
+  for (int n = 1; n <= height; ++n) M2[n] = (uint32_t)(((1ull << 31) + n - 1) / n);
+  // per-row ground model and gravity thresholds (a3)
+  std::vector<int> dgR(height);
+  for (int v = 0; v < height; ++v) dgR[v] = (int)hm.ground_R(v);
+
+  DPArgs& A = h->args;
+  std::memset(&A, 0, sizeof(A));
+  // gravity / diving thresholds on the integer object mean f at base row v:
+  // f*R > dgR + gm*R  <=>  f >= floor((dgR + gm*R)/R) + 1 ;  f*R < dgR - gm*R  <=>
+  // f < ceil((dgR - gm*R)/R).  Packed as clamped u16 pair (unsigned compares).
+  const long long gmR = (long long)params->grav_margin * R;
+  for (int v = 0; v < height; ++v) {
+    long long a1 = floor_div(dgR[v] + gmR, R) + 1;
+    long long bb = ceil_div(dgR[v] - gmR, R);
+    a1 = std::max(0LL, std::min(65535LL, a1));
+    bb = std::max(0LL, std::min(65535LL, bb));
+    A.thr[v] = (uint32_t)a1 | ((uint32_t)bb << 16);
+  }
+  // priors (L#1): each constant quantized on its own
+  const double bic = Host::nl(params->p_exist);
+  double first[3], trans[3][3];
+  for (int c = 0; c < 3; ++c) {
+    first[c] = hm.Q(Host::nl(params->p_first[c]) + bic);
+    for (int d = 0; d < 3; ++d) trans[c][d] = hm.Q(Host::nl(params->p_trans[c][d]) + bic);
+  }
+  const double ord_hi = hm.Q(Host::nl(params->p_ord));
+  const double ord_lo = hm.Q(Host::nl(1.0 - (double)params->p_ord));
+  const double grav_hi = hm.Q(Host::nl(params->p_grav));
+  const double grav_lo = hm.Q(Host::nl(params->p_blg));
+  const double grav_mid = hm.Q(Host::nl(1.0 - (double)params->p_grav - (double)params->p_blg));
+  A.piFirstO = (float)first[1];
+  A.piFirstG = (float)first[0];
+  A.kOO_lo = (float)(trans[1][1] + ord_lo);
+  A.kOO_hi = (float)(trans[1][1] + ord_hi);
+  A.kGO_mid = (float)(trans[0][1] + grav_mid);
+  A.kGO_hi = (float)(trans[0][1] + grav_hi);
+  A.kGO_lo = (float)(trans[0][1] + grav_lo);
+  A.kOG = (float)trans[1][0];
+  A.kGS = (float)trans[0][2];
+  A.kOS = (float)trans[1][2];
+  if (params->cost_frac_bits > 0) {
+    // exact mode: every finite cost must stay an exact fp32 integer (< 2^24)
+    double pmax = 0;
+    double cands[] = {first[0], first[1], trans[0][1] + std::max({grav_hi, grav_lo, grav_mid}),
+                      trans[1][1] + std::max(ord_hi, ord_lo), trans[1][0], trans[0][2], trans[1][2]};
+    for (double c : cands)
+      if (std::isfinite(c)) pmax = std::max(pmax, c);
+    double bound = (double)height * capQ + 4.0 * pmax + (double)height * pmax;
+    if (bound >= 16777216.0)
+      return bail(STIXELS_ERR_UNSUPPORTED,
+                  "exact mode range: h*cap + priors >= 2^24 quanta; lower cost_frac_bits (L#22)");
+  }
+  A.h = height; A.D = D; A.n_cols = h->n_cols; A.cap = h->cap;
+  A.LG = (int)gG.size(); A.LS = (int)gS.size(); A.esz = esz; A.dmr_inv = einv;
+  A.ord_margin = params->ord_margin;
+  A.capQ = (float)capQ;
+  A.cost_scale = params->cost_frac_bits > 0 ? (float)std::ldexp(1.0, -params->cost_frac_bits) : 1.f;
+
+  // ---------------- device ---------------------------------------------------
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return bail(STIXELS_ERR_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+  cudaDeviceProp prop;
+  e = cudaGetDeviceProperties(&prop, device);
+  if (e != cudaSuccess) return bail(STIXELS_ERR_CUDA, std::string("cudaGetDeviceProperties: ") + cudaGetErrorString(e));
+  if (prop.major != 10) return bail(STIXELS_ERR_CUDA, "this library is built for sm_100a (B200) only");
+  h->sms = prop.multiProcessorCount;
+  int optin = (int)prop.sharedMemPerBlockOptin;
+  int cb = DPv == 128 ? col_smem_bytes<128>(height) : col_smem_bytes<256>(height);
+  int sb = al16((height + 1) * 4) + 4 * esz * 4 + al16(kTri * 2);   // M2, E copies, triangle decode
+  int cpc = std::min(4, (optin - sb) / cb);   // columns per CTA (4 warps each)
+  if (cpc < 1) return bail(STIXELS_ERR_UNSUPPORTED, "per-column shared memory exceeds the SM");
+  h->cols_per_cta = cpc;
+  h->smem = sb + cpc * cb;
+  A.col_bytes = cb; A.shared_bytes = sb; A.cols_per_cta = cpc;
+  if (DPv == 128) e = cudaFuncSetAttribute(dp_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem);
+  else e = cudaFuncSetAttribute(dp_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem);
+  if (e != cudaSuccess) return bail(STIXELS_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+  int per_sm = 0;
+  if (DPv == 128) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dp_kernel<128>, cpc * kCW * 32, h->smem);
+  else e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dp_kernel<256>, cpc * kCW * 32, h->smem);
+  if (e != cudaSuccess || per_sm < 1) return bail(STIXELS_ERR_UNSUPPORTED, "dp_kernel does not fit on an SM");
+  h->grid = h->sms * per_sm;
+  // reduction tile
+  h->red_tc = std::max(1, std::min(h->n_cols, 512 / params->stixel_width));
+  h->red_smem = kRedRows * (h->red_tc * params->stixel_width + 1) * 2;
+
+  auto alloc = [&](void** ptr, size_t n) { return cudaMalloc(ptr, n); };
+  if ((e = alloc((void**)&h->d_E, E4.size() * 4)) != cudaSuccess ||
+      (e = alloc((void**)&h->d_M2, M2.size() * 4)) != cudaSuccess ||
+      (e = alloc((void**)&h->d_gG, gG.size() * 4)) != cudaSuccess ||
+      (e = alloc((void**)&h->d_gS, gS.size() * 4)) != cudaSuccess ||
+      (e = alloc((void**)&h->d_dgR, dgR.size() * 4)) != cudaSuccess ||
+      (e = alloc((void**)&h->d_overflow, 4)) != cudaSuccess ||
+      (e = alloc((void**)&h->d_scratch, (size_t)h->grid * cpc * 2 * (height + 1) * 4)) != cudaSuccess ||
+      (e = alloc((void**)&h->d_cols, (size_t)max_batch * h->n_cols * height * 2)) != cudaSuccess)
+    return bail(STIXELS_ERR_CUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+  cudaMemcpy(h->d_E, E4.data(), E4.size() * 4, cudaMemcpyHostToDevice);
+  cudaMemcpy(h->d_M2, M2.data(), M2.size() * 4, cudaMemcpyHostToDevice);
+  cudaMemcpy(h->d_gG, gG.data(), gG.size() * 4, cudaMemcpyHostToDevice);
+  cudaMemcpy(h->d_gS, gS.data(), gS.size() * 4, cudaMemcpyHostToDevice);
+  cudaMemcpy(h->d_dgR, dgR.data(), dgR.size() * 4, cudaMemcpyHostToDevice);
+  cudaMemset(h->d_overflow, 0, 4);
+  e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return bail(STIXELS_ERR_CUDA, std::string("table upload: ") + cudaGetErrorString(e));
+  A.E = h->d_E; A.M2 = h->d_M2; A.gG = h->d_gG; A.gS = h->d_gS; A.dgR = h->d_dgR;
+  A.overflow = h->d_overflow;
+  A.scratch = h->d_scratch;
+  *out = h;
+  return STIXELS_OK;
+}
+
+int stixels_query(const stixels_handle* h, int* n_cols, int* cap) {
+  if (!h) return STIXELS_ERR_ARG;
+  if (n_cols) *n_cols = h->n_cols;
+  if (cap) *cap = h->cap;
+  return STIXELS_OK;
+}
+
+static int launch_reduce(stixels_handle* h, const void* d_disp, int64_t pitch, int batch,
+                         uint16_t* d_cols, cudaStream_t s) {
+  ReduceArgs r;
+  r.disp = (const uint8_t*)d_disp; r.pitch = pitch; r.W = h->W; r.H = h->H; r.n_cols = h->n_cols;
+  r.s = h->p.stixel_width; r.tc = h->red_tc; r.q_bits = h->p.disp_frac_bits; r.D = h->p.max_disparity;
+  r.bpp = h->p.disp_format == STIXELS_U16 ? 2 : 1;
+  r.invalid = h->p.invalid_value;
+  r.out = d_cols;
+  dim3 grid((h->n_cols + h->red_tc - 1) / h->red_tc, (h->H + kRedRows - 1) / kRedRows, batch);
+  reduce_kernel<<<grid, kRedThreads, h->red_smem, s>>>(r);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(h, STIXELS_ERR_CUDA, std::string("reduce_kernel: ") + cudaGetErrorString(e));
+  return STIXELS_OK;
+}
+
+static int launch_dp(stixels_handle* h, const uint16_t* d_cols, int batch, stixel_t* d_out,
+                     int32_t* d_count, float* d_cost, cudaStream_t s) {
+  DPArgs A = h->args;
+  A.cols = d_cols; A.out = d_out; A.count = d_count; A.col_cost = d_cost;
+  A.items = batch * h->n_cols;
+  int grid = std::min(h->grid, (A.items + h->cols_per_cta - 1) / h->cols_per_cta);
+  const int threads = h->cols_per_cta * kCW * 32;
+  if (h->dp_slots == 128) dp_kernel<128><<<grid, threads, h->smem, s>>>(A);
+  else dp_kernel<256><<<grid, threads, h->smem, s>>>(A);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(h, STIXELS_ERR_CUDA, std::string("dp_kernel: ") + cudaGetErrorString(e));
+  return STIXELS_OK;
+}
+
+static int check_disp_args(stixels_handle* h, const void* d, int64_t pitch, int batch) {
+  if (!h) return STIXELS_ERR_ARG;
+  if (h->sticky) return h->sticky;
+  int bpp = h->p.disp_format == STIXELS_U16 ? 2 : 1;
+  if (!d || batch < 1 || batch > h->max_batch || pitch < (int64_t)h->W * bpp || (pitch % bpp))
+    return fail(h, STIXELS_ERR_ARG, "bad input pointer, batch or row pitch");
+  return STIXELS_OK;
+}
+
+int stixels_reduce(stixels_handle* h, const void* d_disp, int64_t pitch, int batch, uint16_t* d_cols) {
+  int st = check_disp_args(h, d_disp, pitch, batch);
+  if (st) return st;
+  if (!d_cols) return fail(h, STIXELS_ERR_ARG, "d_cols is NULL");
+  cudaSetDevice(h->device);
+  h->launches = 1;
+  return launch_reduce(h, d_disp, pitch, batch, d_cols, h->stream);
+}
+
+int stixels_solve(stixels_handle* h, const uint16_t* d_cols, int batch, stixel_t* d_out,
+                  int32_t* d_count, float* d_cost) {
+  if (!h) return STIXELS_ERR_ARG;
+  if (h->sticky) return h->sticky;
+  if (!d_cols || !d_out || !d_count || batch < 1 || batch > h->max_batch)
+    return fail(h, STIXELS_ERR_ARG, "bad pointer or batch");
+  cudaSetDevice(h->device);
+  h->launches = 1;
+  return launch_dp(h, d_cols, batch, d_out, d_count, d_cost, h->stream);
+}
+
+int stixels_compute(stixels_handle* h, const void* d_disp, int64_t pitch, int batch,
+                    stixel_t* d_out, int32_t* d_count, float* d_cost) {
+  int st = check_disp_args(h, d_disp, pitch, batch);
+  if (st) return st;
+  if (!d_out || !d_count) return fail(h, STIXELS_ERR_ARG, "output pointer is NULL");
+  cudaSetDevice(h->device);
+  h->launches = 2;
+  st = launch_reduce(h, d_disp, pitch, batch, h->d_cols, h->stream);
+  if (st) return st;
+  return launch_dp(h, h->d_cols, batch, d_out, d_count, d_cost, h->stream);
+}
+
+int stixels_compute_host(stixels_handle* h, const void* h_disp, int64_t pitch, int batch,
+                         stixel_t* h_out, int32_t* h_count, float* h_cost) {
+  if (!h) return STIXELS_ERR_ARG;
+  if (h->sticky) return h->sticky;
+  int bpp = h->p.disp_format == STIXELS_U16 ? 2 : 1;
+  if (!h_disp || !h_out || !h_count || batch < 1 || pitch < (int64_t)h->W * bpp)
+    return fail(h, STIXELS_ERR_ARG, "bad host pointer, batch or pitch");
+  cudaSetDevice(h->device);
+  const int chunk = std::min(h->max_batch, 64);
+  const size_t in_b = (size_t)h->H * pitch;
+  if (h->h_chunk != chunk || h->h_pitch != pitch) {
+    for (int i = 0; i < 2; ++i) {
+      cudaFree(h->hin[i]); cudaFree(h->hout[i]); cudaFree(h->hcnt[i]); cudaFree(h->hcost[i]);
+      cudaFree(h->hcols[i]);
+      h->hin[i] = nullptr; h->hout[i] = nullptr; h->hcnt[i] = nullptr; h->hcost[i] = nullptr;
+      h->hcols[i] = nullptr;
+      if (!h->hs[i]) CU(cudaStreamCreateWithFlags(&h->hs[i], cudaStreamNonBlocking), h);
+      CU(cudaMalloc(&h->hin[i], in_b * chunk), h);
+      CU(cudaMalloc(&h->hout[i], sizeof(stixel_t) * (size_t)chunk * h->n_cols * h->cap), h);
+      CU(cudaMalloc(&h->hcnt[i], sizeof(int32_t) * (size_t)chunk * h->n_cols), h);
+      CU(cudaMalloc(&h->hcost[i], sizeof(float) * (size_t)chunk * h->n_cols), h);
+      CU(cudaMalloc(&h->hcols[i], 2 * (size_t)chunk * h->n_cols * h->H), h);
+    }
+    h->h_chunk = chunk;
+    h->h_pitch = pitch;
+  }
+  int launches = 0;
+  for (int b0 = 0, it = 0; b0 < batch; b0 += chunk, ++it) {
+    const int nb = std::min(chunk, batch - b0);
+    const int i = it & 1;
+    cudaStream_t s = h->hs[i];
+    const size_t items = (size_t)nb * h->n_cols;
+    CU(cudaMemcpyAsync(h->hin[i], (const uint8_t*)h_disp + (size_t)b0 * in_b, in_b * nb,
+                       cudaMemcpyHostToDevice, s), h);
+    int st = launch_reduce(h, h->hin[i], pitch, nb, h->hcols[i], s);
+    if (st) return st;
+    st = launch_dp(h, h->hcols[i], nb, h->hout[i], h->hcnt[i], h->hcost[i], s);
+    if (st) return st;
+    launches += 2;
+    CU(cudaMemcpyAsync(h_out + (size_t)b0 * h->n_cols * h->cap, h->hout[i],
+                       sizeof(stixel_t) * items * h->cap, cudaMemcpyDeviceToHost, s), h);
+    CU(cudaMemcpyAsync(h_count + (size_t)b0 * h->n_cols, h->hcnt[i], sizeof(int32_t) * items,
+                       cudaMemcpyDeviceToHost, s), h);
+    if (h_cost)
+      CU(cudaMemcpyAsync(h_cost + (size_t)b0 * h->n_cols, h->hcost[i], sizeof(float) * items,
+                         cudaMemcpyDeviceToHost, s), h);
+  }
+  h->launches = launches;
+  CU(cudaStreamSynchronize(h->hs[0]), h);
+  CU(cudaStreamSynchronize(h->hs[1]), h);
+  return stixels_sync(h);
+}
+
+int stixels_sync(stixels_handle* h) {
+  if (!h) return STIXELS_ERR_ARG;
+  cudaSetDevice(h->device);
+  cudaError_t e = cudaStreamSynchronize(h->stream);
+  if (e != cudaSuccess) return fail(h, STIXELS_ERR_CUDA, std::string("sync: ") + cudaGetErrorString(e));
+  int ov = 0;
+  e = cudaMemcpy(&ov, h->d_overflow, 4, cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return fail(h, STIXELS_ERR_CUDA, std::string("sync: ") + cudaGetErrorString(e));
+  if (ov) {
+    cudaMemset(h->d_overflow, 0, 4);
+    return fail(h, STIXELS_ERR_CAPACITY, "a column produced more stixels than max_stixels");
+  }
+  return h->sticky ? h->sticky : STIXELS_OK;
+}
+
+int stixels_last_launch_count(const stixels_handle* h) { return h ? h->launches : 0; }
+
+int stixels_destroy(stixels_handle* h) {
+  if (!h) return STIXELS_OK;
+  cudaSetDevice(h->device);
+  cudaStreamSynchronize(h->stream);
+  free_all(h);
+  delete h;
+  return STIXELS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,168 @@
+"""Parity of the CUDA path (through the C ABI) with the oracle, element by
+element, on the same seeded inputs.  Exact mode (L#22): identical stixel lists
+and identical column costs on EVERY column.  Continuous mode: BASELINE
+north_star tolerance (column cost within 1e-4 relative; identical lists except
+on columns whose GPU segmentation re-scores within 1e-4 of the oracle minimum).
+"""
+import numpy as np
+import pytest
+
+from inputs import synth
+from tests import modelparams as mp
+from tests.gpuharness import compare_exact, run_gpu, run_oracle
+
+pytestmark = pytest.mark.gpu
+
+
+def _frames_c2(n, seed0=2000, W=1024, H=440, D=128):
+    return np.stack([synth.render(synth.random_scene(seed0 + i, W, H, D), seed0 + i)
+                     for i in range(n)])
+
+
+def _assert_exact(p, frames, **kw):
+    g, gc, cnt, hd = run_gpu(p, frames, **kw)
+    o, oc = run_oracle(p, frames)
+    bad = compare_exact(g, gc, o, oc, p["cost_frac_bits"])
+    assert not bad, f"{len(bad)} mismatching columns, first: {bad[:2]}"
+    return g, gc, cnt, hd
+
+
+def test_reduce_bit_exact():
+    import torch
+    from oracle import oracle as orc
+    from paper_1610_04124_b200 import stixels as S
+    frames = _frames_c2(3, W=1027)          # ragged tail: 1027 mod 5 = 2 dropped
+    p = mp.make()
+    B, H, W = frames.shape
+    hd = S.Handle(S.params_from_dict(p, H), W, H, B)
+    cols = torch.empty((B, hd.n_cols, H), dtype=torch.int16, device="cuda")   # u16 storage
+    hd.reduce(torch.from_numpy(frames.view(np.int16)).cuda(), cols)
+    hd.sync()
+    got = cols.cpu().numpy().view(np.uint16).astype(np.int32)
+    got[got == 0xFFFF] = -1
+    for b in range(B):
+        want = orc.reduce(frames[b], 5, 4, 0xFFFF, 128)
+        assert (got[b] == want).all()
+
+
+def test_c1_scene_exact():
+    sc = synth.c1_scene()
+    frames = np.stack([synth.render(sc, 1, noise=False), synth.render(sc, 2)])
+    p = mp.make(max_disparity=32, ground_slope=sc.alpha)
+    _assert_exact(p, frames)
+
+
+def test_c2_frames_exact():
+    frames = _frames_c2(3)
+    p = mp.make()
+    g, gc, cnt, hd = _assert_exact(p, frames)
+    assert hd.last_launch_count() == 2
+
+
+@pytest.mark.parametrize("H,W,D,s", [(1, 40, 16, 5), (31, 64, 16, 3), (32, 50, 64, 5),
+                                     (33, 61, 128, 1), (65, 96, 200, 7), (100, 70, 256, 10)])
+def test_shapes_and_disparity_ranges_exact(H, W, D, s):
+    """Ragged column heights (1, 31, 32, 33, 65: partial 32-row blocks), D up to
+    256 (the 256-slot kernel), s in {1,3,5,7,10}, ragged widths."""
+    frames = np.stack([synth.uniform_random_image(77 + i, W, H, D) for i in range(2)] +
+                      [synth.render(synth.random_scene(90, W, H, D, alpha=0.9 * D / max(H, 2)),
+                                    90)])
+    p = mp.make(max_disparity=D, stixel_width=s, ground_slope=0.9 * D / max(H, 2))
+    _assert_exact(p, frames)
+
+
+def test_degenerate_columns_exact():
+    """All-invalid frame, all-zero frame, saturated (d = D - 1/16) frame."""
+    H, W, D = 70, 40, 64
+    f0 = np.full((H, W), 0xFFFF, np.uint16)
+    f1 = np.zeros((H, W), np.uint16)
+    f2 = np.full((H, W), D * 16 - 1, np.uint16)
+    p = mp.make(max_disparity=D)
+    _assert_exact(p, np.stack([f0, f1, f2]))
+
+
+def test_u8_input_exact():
+    H, W, D = 120, 100, 64
+    rng = np.random.default_rng(8)
+    sc = synth.random_scene(8, W, H, D, alpha=0.5, q_bits=2)
+    f16 = synth.render(sc, 8)
+    f8 = np.where(f16 == 0xFFFF, 255, np.minimum(f16, 254)).astype(np.uint8)
+    p = mp.make(max_disparity=D, disp_frac_bits=2, invalid_value=255, ground_slope=0.5)
+    _assert_exact(p, f8[None])
+
+
+def test_random_priors_exact():
+    """Random (structurally valid) prior weights, margins and sigmas."""
+    rng = np.random.default_rng(12)
+    H, W, D = 96, 80, 48
+    for it in range(4):
+        t = mp.default_trans()
+        for a, b in [(0, 1), (0, 2), (1, 0), (1, 1), (1, 2)]:
+            t[a][b] = float(rng.choice([1.0, 0.3, 0.05, 0.0]))
+        p = mp.make(max_disparity=D, p_trans=t, p_ord=float(rng.uniform(0.01, 0.5)),
+                    p_grav=float(rng.uniform(0, 0.4)), p_blg=float(rng.uniform(0, 0.4)),
+                    p_exist=float(rng.choice([1.0, 0.1, 0.01])),
+                    p_first=(1.0, float(rng.choice([1.0, 0.1, 0.0])), 0.0),
+                    ord_margin=int(rng.integers(0, 4)), grav_margin=int(rng.integers(0, 4)),
+                    sigma=tuple(float(x) for x in rng.choice([0.5, 1.0, 1.5, 3.0], 3)),
+                    ground_slope=float(rng.uniform(0.2, 0.8)), cost_frac_bits=int(rng.integers(6, 12)))
+        frames = np.stack([synth.render(synth.random_scene(300 + it, W, H, D, alpha=p["ground_slope"]),
+                                        300 + it), synth.uniform_random_image(400 + it, W, H, D)])
+        _assert_exact(p, frames)
+
+
+def test_continuous_mode_tolerance():
+    """cost_frac_bits = 0: fp32 Eq. 4 vs double.  Column cost within 1e-4
+    relative; lists identical except where the GPU's segmentation is co-optimal
+    (re-scored within 1e-4 of the oracle minimum), BASELINE north_star."""
+    from oracle import oracle as orc
+    frames = _frames_c2(1)
+    p = mp.make(cost_frac_bits=0)
+    g, gc, cnt, hd = run_gpu(p, frames)
+    o, oc = run_oracle(p, frames)
+    m = mp.oracle_model(p, 440)
+    cols = orc.reduce(frames[0], 5, 4, 0xFFFF, 128)
+    ties = 0
+    for c in range(len(o[0])):
+        assert abs(gc[0][c] - oc[0][c]) <= 1e-4 * abs(oc[0][c])
+        og = [(a, b, k) for a, b, k, _ in o[0][c]]
+        gg = [(a, b, k) for a, b, k, _ in g[0][c]]
+        if og != gg:
+            ties += 1
+            rs = orc.rescore(m, cols[c], [(a, b, k, 0.0) for a, b, k in gg])
+            assert abs(rs - oc[0][c]) <= 1e-4 * abs(oc[0][c])
+    assert ties <= len(o[0]) // 10
+
+
+def test_capacity_overflow_reported():
+    from paper_1610_04124_b200 import stixels as S
+    frames = _frames_c2(1)
+    p = mp.make(max_stixels=3)
+    with pytest.raises(S.StixelsError) as ei:
+        run_gpu(p, frames)
+    assert ei.value.status == S.ERR_CAPACITY
+
+
+def test_host_path_matches_device_path():
+    frames = _frames_c2(70, seed0=5000, W=200, H=150)   # > one 64-frame chunk
+    p = mp.make(ground_slope=0.6)
+    a, ac, an, _ = run_gpu(p, frames)
+    b, bc, bn, _ = run_gpu(p, frames, host=True)
+    assert a == b and (ac == bc).all() and (an == bn).all()
+
+
+def test_deterministic_bytes():
+    import torch
+    from paper_1610_04124_b200 import stixels as S
+    frames = _frames_c2(2)
+    p = mp.make()
+    params = S.params_from_dict(p, 440)
+    hd = S.Handle(params, 1024, 440, 2)
+    t = torch.from_numpy(frames.view(np.int16)).cuda()
+    o1, c1, k1 = hd.alloc_outputs(2)
+    o2, c2, k2 = hd.alloc_outputs(2)
+    o1.zero_(); o2.zero_()
+    hd.compute(t, o1, c1, k1)
+    hd.compute(t, o2, c2, k2)
+    hd.sync()
+    assert torch.equal(o1, o2) and torch.equal(c1, c2) and torch.equal(k1, k2)
