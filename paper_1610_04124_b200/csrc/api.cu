@@ -25,6 +25,7 @@ struct stixels_handle {
   int W = 0, H = 0, max_batch = 0, device = 0;
   cudaStream_t stream = nullptr;
   int n_cols = 0, cap = 0, dp_slots = 128, cols_per_cta = 0, smem = 0, grid = 0, sms = 0;
+  bool sparse = true;
   int red_tc = 0, red_smem = 0;
   DPArgs args{};
   float* d_E = nullptr;
@@ -32,6 +33,7 @@ struct stixels_handle {
   float* d_gG = nullptr;
   float* d_gS = nullptr;
   int* d_dgR = nullptr;
+  uint32_t* d_thr = nullptr;
   int* d_overflow = nullptr;
   float* d_scratch = nullptr;
   uint16_t* d_cols = nullptr;
@@ -207,7 +209,7 @@ const char* stixels_last_error(const stixels_handle* h) {
 
 static void free_all(stixels_handle* h) {
   cudaFree(h->d_E); cudaFree(h->d_M2); cudaFree(h->d_gG); cudaFree(h->d_gS);
-  cudaFree(h->d_dgR); cudaFree(h->d_overflow); cudaFree(h->d_cols); cudaFree(h->d_scratch);
+  cudaFree(h->d_dgR); cudaFree(h->d_thr); cudaFree(h->d_overflow); cudaFree(h->d_cols); cudaFree(h->d_scratch);
   for (int i = 0; i < 2; ++i) {
     cudaFree(h->hin[i]); cudaFree(h->hout[i]); cudaFree(h->hcnt[i]); cudaFree(h->hcost[i]);
     cudaFree(h->hcols[i]);
@@ -258,16 +260,24 @@ int stixels_create(const stixels_params* params, int width, int height, int max_
   }
   gG.back() = (float)capQ;   // clamp index -> cap (monotone Eq. 4)
   gS.back() = (float)capQ;
-  // object pair-cost LUT Pair[f][d] = Eq4(d - f, sigma_O) as E[f - d + D]
+  // object pair-cost LUT Pair[f][d] = Eq4(d - f, sigma_O), stored shifted by
+  // the outlier cap as E'[f - d + D] = Pair - cap (<= 0, exact integers in exact
+  // mode): the DP kernel works with W-rows LUT_object[f][v] - cap * v.
   const int DPv = h->dp_slots;
   const int einv = ((D + DPv + 4) + 3) & ~3;
   const int esz = einv + DPv + 8;
   std::vector<float> E1((size_t)esz + 8);
   for (int i = 0; i < esz + 8; ++i)
-    E1[i] = (i < einv) ? (float)hm.Q(hm.eq4((double)(i - D), (double)params->sigma[1])) : (float)capQ;
+    E1[i] = (i < einv) ? (float)(hm.Q(hm.eq4((double)(i - D), (double)params->sigma[1])) - capQ) : 0.f;
   std::vector<float> E4((size_t)4 * esz);
   for (int c = 0; c < 4; ++c)
     for (int i = 0; i < esz; ++i) E4[(size_t)c * esz + i] = E1[i + c];
+  // band of the pair cost: |f - d| beyond which Pair == cap.  If <= 7 the kernel
+  // updates W-rows sparsely (wt[d + 7] = cap - Pair for |d| <= 7).
+  int band = 0;
+  for (int d = -D; d <= D; ++d)
+    if (E1[d + D] != 0.f) band = std::max(band, std::abs(d));
+  const bool sparse = band <= 7;
   // magic reciprocals: floor(y/(2n)) = umulhi(y, ceil(2^31/n))
   std::vector<uint32_t> M2(height + 1);
   M2[0] = 0;
@@ -282,13 +292,18 @@ int stixels_create(const stixels_params* params, int width, int height, int max_
   // f*R > dgR + gm*R  <=>  f >= floor((dgR + gm*R)/R) + 1 ;  f*R < dgR - gm*R  <=>
   // f < ceil((dgR - gm*R)/R).  Packed as clamped u16 pair (unsigned compares).
   const long long gmR = (long long)params->grav_margin * R;
+  std::vector<uint32_t> thrg(height);
   for (int v = 0; v < height; ++v) {
     long long a1 = floor_div(dgR[v] + gmR, R) + 1;
     long long bb = ceil_div(dgR[v] - gmR, R);
-    a1 = std::max(0LL, std::min(65535LL, a1));
-    bb = std::max(0LL, std::min(65535LL, bb));
-    A.thr[v] = (uint32_t)a1 | ((uint32_t)bb << 16);
+    a1 = std::max(0LL, std::min(1023LL, a1));     // f <= 255 < 1023: clamping is exact
+    bb = std::max(0LL, std::min(1023LL, bb));
+    A.thrA1[v] = (int)a1;
+    A.thrB[v] = (int)bb;
+    thrg[v] = (uint32_t)a1 | ((uint32_t)bb << 16);
   }
+  for (int d = -7; d <= 7; ++d) A.wt[d + 7] = sparse ? -E1[d + D] : 0.f;
+  A.wt[15] = 0.f;
   // priors (L#1): each constant quantized on its own
   const double bic = Host::nl(params->p_exist);
   double first[3], trans[3][3];
@@ -318,11 +333,16 @@ int stixels_create(const stixels_params* params, int width, int height, int max_
                       trans[1][1] + std::max(ord_hi, ord_lo), trans[1][0], trans[0][2], trans[1][2]};
     for (double c : cands)
       if (std::isfinite(c)) pmax = std::max(pmax, c);
-    double bound = (double)height * capQ + 4.0 * pmax + (double)height * pmax;
+    // Every finite intermediate is bounded by h*cap + 4*pmax: C values are minima,
+    // hence at most the cost of a one- or two-stixel segmentation; W-row
+    // differences P_k - W_j are sums of at most h terms in [-cap, 0]; shifted
+    // predecessor terms C[j-1] + t - cap*j lie in [-cap*h, 4*pmax].
+    double bound = (double)height * capQ + 4.0 * pmax;
     if (bound >= 16777216.0)
       return bail(STIXELS_ERR_UNSUPPORTED,
                   "exact mode range: h*cap + priors >= 2^24 quanta; lower cost_frac_bits (L#22)");
   }
+  h->sparse = sparse;
   A.h = height; A.D = D; A.n_cols = h->n_cols; A.cap = h->cap;
   A.LG = (int)gG.size(); A.LS = (int)gS.size(); A.esz = esz; A.dmr_inv = einv;
   A.ord_margin = params->ord_margin;
@@ -338,19 +358,22 @@ int stixels_create(const stixels_params* params, int width, int height, int max_
   if (prop.major != 10) return bail(STIXELS_ERR_CUDA, "this library is built for sm_100a (B200) only");
   h->sms = prop.multiProcessorCount;
   int optin = (int)prop.sharedMemPerBlockOptin;
-  int cb = DPv == 128 ? col_smem_bytes<128>(height) : col_smem_bytes<256>(height);
+  auto kfun = [&]() -> const void* {
+    if (DPv == 128) return sparse ? (const void*)dp_kernel<128, true> : (const void*)dp_kernel<128, false>;
+    return sparse ? (const void*)dp_kernel<256, true> : (const void*)dp_kernel<256, false>;
+  };
+  int cb = DPv == 128 ? (sparse ? col_smem_bytes<128, true>(height) : col_smem_bytes<128, false>(height))
+                      : (sparse ? col_smem_bytes<256, true>(height) : col_smem_bytes<256, false>(height));
   int sb = al16((height + 1) * 4) + 4 * esz * 4 + al16(kTri * 2);   // M2, E copies, triangle decode
   int cpc = std::min(4, (optin - sb) / cb);   // columns per CTA (4 warps each)
   if (cpc < 1) return bail(STIXELS_ERR_UNSUPPORTED, "per-column shared memory exceeds the SM");
   h->cols_per_cta = cpc;
   h->smem = sb + cpc * cb;
   A.col_bytes = cb; A.shared_bytes = sb; A.cols_per_cta = cpc;
-  if (DPv == 128) e = cudaFuncSetAttribute(dp_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem);
-  else e = cudaFuncSetAttribute(dp_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem);
+  e = cudaFuncSetAttribute(kfun(), cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem);
   if (e != cudaSuccess) return bail(STIXELS_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
   int per_sm = 0;
-  if (DPv == 128) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dp_kernel<128>, cpc * kCW * 32, h->smem);
-  else e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dp_kernel<256>, cpc * kCW * 32, h->smem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfun(), cpc * kCW * 32, h->smem);
   if (e != cudaSuccess || per_sm < 1) return bail(STIXELS_ERR_UNSUPPORTED, "dp_kernel does not fit on an SM");
   h->grid = h->sms * per_sm;
   // reduction tile
@@ -363,8 +386,10 @@ int stixels_create(const stixels_params* params, int width, int height, int max_
       (e = alloc((void**)&h->d_gG, gG.size() * 4)) != cudaSuccess ||
       (e = alloc((void**)&h->d_gS, gS.size() * 4)) != cudaSuccess ||
       (e = alloc((void**)&h->d_dgR, dgR.size() * 4)) != cudaSuccess ||
+      (e = alloc((void**)&h->d_thr, thrg.size() * 4)) != cudaSuccess ||
       (e = alloc((void**)&h->d_overflow, 4)) != cudaSuccess ||
-      (e = alloc((void**)&h->d_scratch, (size_t)h->grid * cpc * 2 * (height + 1) * 4)) != cudaSuccess ||
+      (e = alloc((void**)&h->d_scratch, (size_t)h->grid * cpc * 4 *
+                        (DPv == 128 ? col_scratch_floats<128>(height) : col_scratch_floats<256>(height)))) != cudaSuccess ||
       (e = alloc((void**)&h->d_cols, (size_t)max_batch * h->n_cols * height * 2)) != cudaSuccess)
     return bail(STIXELS_ERR_CUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e));
   cudaMemcpy(h->d_E, E4.data(), E4.size() * 4, cudaMemcpyHostToDevice);
@@ -372,10 +397,11 @@ int stixels_create(const stixels_params* params, int width, int height, int max_
   cudaMemcpy(h->d_gG, gG.data(), gG.size() * 4, cudaMemcpyHostToDevice);
   cudaMemcpy(h->d_gS, gS.data(), gS.size() * 4, cudaMemcpyHostToDevice);
   cudaMemcpy(h->d_dgR, dgR.data(), dgR.size() * 4, cudaMemcpyHostToDevice);
+  cudaMemcpy(h->d_thr, thrg.data(), thrg.size() * 4, cudaMemcpyHostToDevice);
   cudaMemset(h->d_overflow, 0, 4);
   e = cudaDeviceSynchronize();
   if (e != cudaSuccess) return bail(STIXELS_ERR_CUDA, std::string("table upload: ") + cudaGetErrorString(e));
-  A.E = h->d_E; A.M2 = h->d_M2; A.gG = h->d_gG; A.gS = h->d_gS; A.dgR = h->d_dgR;
+  A.E = h->d_E; A.M2 = h->d_M2; A.gG = h->d_gG; A.gS = h->d_gS; A.dgR = h->d_dgR; A.thrg = h->d_thr;
   A.overflow = h->d_overflow;
   A.scratch = h->d_scratch;
   *out = h;
@@ -411,8 +437,13 @@ static int launch_dp(stixels_handle* h, const uint16_t* d_cols, int batch, stixe
   A.items = batch * h->n_cols;
   int grid = std::min(h->grid, (A.items + h->cols_per_cta - 1) / h->cols_per_cta);
   const int threads = h->cols_per_cta * kCW * 32;
-  if (h->dp_slots == 128) dp_kernel<128><<<grid, threads, h->smem, s>>>(A);
-  else dp_kernel<256><<<grid, threads, h->smem, s>>>(A);
+  if (h->dp_slots == 128) {
+    if (h->sparse) dp_kernel<128, true><<<grid, threads, h->smem, s>>>(A);
+    else dp_kernel<128, false><<<grid, threads, h->smem, s>>>(A);
+  } else {
+    if (h->sparse) dp_kernel<256, true><<<grid, threads, h->smem, s>>>(A);
+    else dp_kernel<256, false><<<grid, threads, h->smem, s>>>(A);
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(h, STIXELS_ERR_CUDA, std::string("dp_kernel: ") + cudaGetErrorString(e));
   return STIXELS_OK;

@@ -130,6 +130,7 @@ struct DPArgs {
   const float* gG;         // ground cost by |dR - dgR|, length LG (last = cap)
   const float* gS;         // sky cost by dR, length LS (last = cap)
   const int* dgR;          // [h] ground model, 1/256 units
+  const uint32_t* thrg;    // [h] thrA1 | thrB << 16 (global copy for divergent reads)
   int* overflow;
   int h, D, n_cols, items, cap, LG, LS, esz, dmr_inv, ord_margin, cols_per_cta;
   int col_bytes, shared_bytes;   // smem layout
@@ -138,26 +139,26 @@ struct DPArgs {
   float kOO_lo, kOO_hi;          // O above O: trans + ordering (lo: no violation)
   float kGO_mid, kGO_hi, kGO_lo; // O above G: trans + gravity level
   float kOG, kGS, kOS;           // G above O, S above G, S above O
-  uint32_t thr[kMaxH];           // per row j: (thrA[j]+1) | thrB[j] << 16, both
-                                 // clamped to [0, 65535]: f >= lo16 <=> floating,
-                                 // f < hi16 <=> below ground (unsigned compares)
+  float wt[16];                  // sparse W-row update: cap - Pair(d) for d = -7..7
+  int thrA1[kMaxH];              // per row j: f >= thrA1[j] <=> floating object at base j
+  int thrB[kMaxH];               //            f <  thrB[j]  <=> object below ground at base j
 };
 
 struct ColSmem {
   float* priv;      // [32][DP+1]     priv[i][f] = LUT_object[f][32b+i+1] of the block being built
-  float* seed;      // [2][2][DP]     LUT rows 32b+12, 32b+24 of block b (parity b & 1)
-  float* anchor;    // [nb+1][DP]     anchor[m][f] = LUT_object[f][32m]
-  float* ring;      // [3][4][DP]     rectangle warps' rings of LUT_object[.][j]
+  float* seed;      // [2][3][DP]     LUT rows 32b+8, +16, +24 of block b (parity b & 1)
+  float* ring;      // [4][RR][DP]    per-warp W-rows W_j = LUT_object[.][j] - cap*j (RR = 2 sparse, 4 dense)
   float* cbd;       // [496]          triangle cells (bottom K0+1+j', target K0+k' > j'), packed
   uint16_t* cbf;    // [496]          ... f | gravity level << 12
-  uint4* rec;       // [h+1][2]       row j: {AO0,AO1,AGm,AGh} {AGl, T[j], N4[j]|ordthr<<16, thr}
+  uint4* rec;       // [h+3][2]       row j: {AO0,AO1,AGm,AGh} {AGl, T[j], N4[j], ordthr | drp<<16}
   uint32_t* eo;     // [h+2]          lo16: ring window byte offset; hi16: E0 byte offset
   uint16_t* argO;   // [h]            j | c'<<12
   uint16_t* argG;   // [h]            j (pred class O, or start if j == 0)
   uint16_t* argS;   // [h]            j | c'<<12
   uint8_t* fpv;     // [h]            f of the last stixel of the best O-ending segmentation
-  float2* part;     // [3][32]        rectangle partial minima {cost, argj}
+  float2* part;     // [4][32]        partial minima {cost, argj} of the 4 warps
   float4* pgps;     // [32]           serial warp: {PG[k], PG[k+1], PS[k], PS[k+1]}
+  int* ctr;         // [1]            dynamic chunk counter
 };
 
 constexpr int kTri = 496;              // cells of a 32-row triangle: sum_{j'<31} (31 - j')
@@ -165,42 +166,47 @@ __host__ __device__ constexpr int tri_off(int jp) { return 31 * jp - (jp * (jp -
 
 __host__ __device__ inline int al16(int x) { return (x + 15) & ~15; }
 
-template <int DP>
+template <int DP, bool SPARSE>
 __host__ __device__ inline int col_smem_bytes(int h) {
-  const int nb = (h + 31) >> 5;
+  constexpr int RR = SPARSE ? 2 : 4;
   int b = 0;
   b += al16(32 * (DP + 1) * 4);
-  b += al16(4 * DP * 4);
-  b += al16((nb + 1) * DP * 4);
-  b += al16(3 * 4 * DP * 4);                      // rings, then cells (contiguous:
-  b += al16(kTri * 4) + al16(kTri * 2);           //  prologue temporaries reuse both)
-  b += al16((h + 1) * 32);
+  b += al16(6 * DP * 4);
+  b += al16(kCW * RR * DP * 4);
+  b += al16(kTri * 4) + al16(kTri * 2);
+  b += al16((h + 3) * 32);
   b += al16((h + 2) * 4);
   b += al16(h * 2) * 3;
   b += al16(h);
-  b += al16(3 * 32 * 8);
+  b += al16(kCW * 32 * 8);
   b += al16(32 * 16);
+  b += 16;
   return b;
 }
-
+// global scratch per column slot: PG[h+1], PS[h+1], anchor rows [nb+1][DP]
 template <int DP>
+__host__ __device__ inline int64_t col_scratch_floats(int h) {
+  return 2 * (int64_t)(h + 1) + (int64_t)(((h + 31) >> 5) + 1) * DP;
+}
+
+template <int DP, bool SPARSE>
 __device__ inline ColSmem carve(uint8_t* p, int h) {
-  const int nb = (h + 31) >> 5;
+  constexpr int RR = SPARSE ? 2 : 4;
   ColSmem w;
   w.priv = reinterpret_cast<float*>(p); p += al16(32 * (DP + 1) * 4);
-  w.seed = reinterpret_cast<float*>(p); p += al16(4 * DP * 4);
-  w.anchor = reinterpret_cast<float*>(p); p += al16((nb + 1) * DP * 4);
-  w.ring = reinterpret_cast<float*>(p); p += al16(3 * 4 * DP * 4);
+  w.seed = reinterpret_cast<float*>(p); p += al16(6 * DP * 4);
+  w.ring = reinterpret_cast<float*>(p); p += al16(kCW * RR * DP * 4);
   w.cbd = reinterpret_cast<float*>(p); p += al16(kTri * 4);
   w.cbf = reinterpret_cast<uint16_t*>(p); p += al16(kTri * 2);
-  w.rec = reinterpret_cast<uint4*>(p); p += al16((h + 1) * 32);
+  w.rec = reinterpret_cast<uint4*>(p); p += al16((h + 3) * 32);
   w.eo = reinterpret_cast<uint32_t*>(p); p += al16((h + 2) * 4);
   w.argO = reinterpret_cast<uint16_t*>(p); p += al16(h * 2);
   w.argG = reinterpret_cast<uint16_t*>(p); p += al16(h * 2);
   w.argS = reinterpret_cast<uint16_t*>(p); p += al16(h * 2);
   w.fpv = p; p += al16(h);
-  w.part = reinterpret_cast<float2*>(p); p += al16(3 * 32 * 8);
-  w.pgps = reinterpret_cast<float4*>(p);
+  w.part = reinterpret_cast<float2*>(p); p += al16(kCW * 32 * 8);
+  w.pgps = reinterpret_cast<float4*>(p); p += al16(32 * 16);
+  w.ctr = reinterpret_cast<int*>(p);
   return w;
 }
 
@@ -243,7 +249,7 @@ __device__ __forceinline__ void named_bar(int id, int threads) {
 // Object model value f of span [j, k] from prefix differences:
 // f = floor(t / (256 n)), t = sum(d + 128) over valid pixels: the exact half-up
 // rounded mean (L#10), via a multiply-high by ceil(2^31/n) (exact for t < 2^28),
-// clamped to D-1.  M2 sits at shared offset 0; n4 = 4n is its byte offset.
+// clamped to D-1.  n4 = 4n is the byte offset into M2 (at the start of dynamic smem).
 __device__ __forceinline__ int span_f(uint32_t t, uint32_t n4, const uint8_t* smem0, int Dm1) {
   uint32_t y = t >> (kRBits - 1);
   uint32_t M = *reinterpret_cast<const uint32_t*>(smem0 + n4);
@@ -264,39 +270,57 @@ __device__ __forceinline__ float ldsf(uint32_t addr) {
 
 // Per-row uniform values of record j for the cell evaluation.
 struct RowU {
-  float AO0, AO1, AGm, AGh, AGl;
+  float AO0, AO1, AGm, AGh, AGl;   // predecessor terms of row j, shifted by -cap*j
   uint32_t T, N4;
-  int ordthr, thrA1, thrB;
+  int ordthr, drp;                 // drp = round(d_j) + 1, 0 if pixel j is invalid
 };
+__device__ __forceinline__ RowU unpack_row(uint4 x, uint4 y) {
+  RowU u;
+  u.AO0 = __uint_as_float(x.x); u.AO1 = __uint_as_float(x.y);
+  u.AGm = __uint_as_float(x.z); u.AGh = __uint_as_float(x.w);
+  u.AGl = __uint_as_float(y.x);
+  u.T = y.y; u.N4 = y.z; u.ordthr = (int)(y.w & 0xffffu); u.drp = (int)(y.w >> 16);
+  return u;
+}
 __device__ __forceinline__ RowU load_row(const uint4* rec, int j) {
   const uint32_t ra = (uint32_t)__cvta_generic_to_shared(rec + 2 * j);
-  uint4 x = lds128(ra), y = lds128(ra + 16);
-  RowU u;
-  u.AO0 = __uint_as_float(x.x); u.AO1 = __uint_as_float(x.y);
-  u.AGm = __uint_as_float(x.z); u.AGh = __uint_as_float(x.w);
-  u.AGl = __uint_as_float(y.x);
-  u.T = y.y; u.N4 = y.z & 0xffffu; u.ordthr = (int)(y.z >> 16);
-  u.thrA1 = (int)(y.w & 0xffffu); u.thrB = (int)(y.w >> 16);
-  return u;
+  return unpack_row(lds128(ra), lds128(ra + 16));
 }
-
 // Plain (compiler-visible) version: records are read-only while a rectangle runs.
 __device__ __forceinline__ RowU load_row_c(const uint4* rec, int j) {
-  const uint4 x = rec[2 * j], y = rec[2 * j + 1];
-  RowU u;
-  u.AO0 = __uint_as_float(x.x); u.AO1 = __uint_as_float(x.y);
-  u.AGm = __uint_as_float(x.z); u.AGh = __uint_as_float(x.w);
-  u.AGl = __uint_as_float(y.x);
-  u.T = y.y; u.N4 = y.z & 0xffffu; u.ordthr = (int)(y.z >> 16);
-  u.thrA1 = (int)(y.w & 0xffffu); u.thrB = (int)(y.w >> 16);
-  return u;
+  return unpack_row(rec[2 * j], rec[2 * j + 1]);
+}
+template <typename T>
+__device__ __forceinline__ T* shp(uint32_t a) {     // shared u32 address -> pointer
+  return reinterpret_cast<T*>(__cvta_shared_to_generic(a));
 }
 
-template <int DP>
+// Packed fp32x2 add (sm_100 FADD2): two independent adds in one instruction.
+__device__ __forceinline__ void fadd2_inplace(float& a0, float& a1, float b0, float b1) {
+  unsigned long long x, y, z;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(x) : "f"(a0), "f"(a1));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(y) : "f"(b0), "f"(b1));
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(z) : "l"(x), "l"(y));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a0), "=f"(a1) : "l"(z));
+}
+
+// ---------------------------------------------------------------------------
+// W-rows.  The kernel never stores LUT_object[f][v] itself but the shifted row
+// W[f][v] = LUT_object[f][v] - cap * v = -sum_{u<v} (cap - Pair[f][d_u]), whose
+// increments are zero except within +-band of the pixel's disparity (Eq. 4 hits
+// the outlier cap): an object span's data term is
+//   LUT[f][k+1] - LUT[f][j] = W[f][k+1] - W[f][j] + cap * (k+1-j).
+// The per-target constant cap*(k+1) is dropped from rectangle candidates (it
+// does not change the argmin over bottoms of one target) and the per-bottom
+// constant -cap*j is folded into the bottom's record.  All values stay exact
+// integers in exact mode (|.| <= 2 h cap < 2^24, checked on the host).
+// ---------------------------------------------------------------------------
+template <int DP, bool SPARSE>
 __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_constant__ DPArgs a) {
   constexpr int NR = DP / 128;         // LDS.128 ring windows per lane
   constexpr int NS = DP / 32;          // 32-wide f slices
   constexpr int NSW = (NS + 2) / 3;    // f slices per rectangle warp (at most)
+  constexpr int RR = SPARSE ? 2 : 4;   // W-rows per warp
   extern __shared__ __align__(16) uint8_t smem[];
   const int lane = threadIdx.x & 31;
   const int wid = threadIdx.x >> 5;
@@ -317,11 +341,14 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
   const int h = a.h;
   const int Dm1 = a.D - 1;
   const int nb = (h + 31) >> 5;
+  const float capQ = a.capQ;
   const int bar_col = 1 + cslot;       // 128 threads: whole column group
   const int bar_rect = 1 + C + cslot;  // 96 threads: rectangle warps
+  const int bar_x = 1 + 2 * C + cslot; // 96 arrive + 32 sync: next block's priv rows ready
 
   // CTA-shared tables: M2 at offset 0, then 4 shifted copies of the object
-  // pair-cost window E (Pair[f][d] = E[f - d + D]).
+  // pair-cost window E' (Pair[f][d] - cap = E'[f - d + D]), then the
+  // triangle cell decode table.
   uint32_t* M2s = reinterpret_cast<uint32_t*>(smem);
   float* E = reinterpret_cast<float*>(smem + al16((h + 1) * 4));
   uint16_t* tri_jk = reinterpret_cast<uint16_t*>(smem + al16((h + 1) * 4) + 4 * a.esz * 4);
@@ -333,112 +360,220 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
   __syncthreads();
   const uint8_t* Eb = reinterpret_cast<const uint8_t*>(E);
 
-  ColSmem cs = carve<DP>(smem + a.shared_bytes + cslot * a.col_bytes, h);
-  float* ringw = cs.ring + (rw < 0 ? 0 : rw) * 4 * DP;
+  ColSmem cs = carve<DP, SPARSE>(smem + a.shared_bytes + cslot * a.col_bytes, h);
+  float* ringw = cs.ring + w * RR * DP;
   const float INF = __int_as_float(0x7f800000);
   const int slot_global = blockIdx.x * a.cols_per_cta + cslot;
-  float* PGg = a.scratch + (int64_t)slot_global * 2 * (h + 1);
+  float* PGg = a.scratch + (int64_t)slot_global * col_scratch_floats<DP>(h);
   float* PSg = PGg + (h + 1);
+  float* ANg = PSg + (h + 1);          // anchor W-rows W[.][32m], global (L2)
 
-  // ---- rectangle-warp helpers ---------------------------------------------
-  // one ring step: rr += Pair[.][d_src] for f = 4*lane.. (+128 r); store to slot
+  // sparse update lanes: lanes 0-14 serve W-row buffer 1 (odd bottoms), lanes
+  // 16-30 buffer 0 (even bottoms); each owns one offset d = (lane & 15) - 7 of
+  // the band and its weight cap - Pair(d)
+  const int boff = (lane & 15) - 7;
+  const float bwt = a.wt[lane & 15];
+  const bool blive = (lane & 15) < 15 && bwt != 0.f;
+  // ---- helpers --------------------------------------------------------------
+  // dense W-row step: rr += E'[.][d_src] for f = 4*lane.. (+128 r); store to slot
   auto ring_step = [&](float (&rr)[4 * NR], int row_src, int slot) {
     uint32_t e = cs.eo[row_src] & 0xffffu;
 #pragma unroll
     for (int r = 0; r < NR; ++r) {
       float4 x = *reinterpret_cast<const float4*>(Eb + e + 16 * lane + 512 * r);
-      rr[4 * r + 0] += x.x; rr[4 * r + 1] += x.y; rr[4 * r + 2] += x.z; rr[4 * r + 3] += x.w;
+      fadd2_inplace(rr[4 * r + 0], rr[4 * r + 1], x.x, x.y);
+      fadd2_inplace(rr[4 * r + 2], rr[4 * r + 3], x.z, x.w);
       *reinterpret_cast<float4*>(ringw + slot * DP + 4 * lane + 128 * r) =
           make_float4(rr[4 * r + 0], rr[4 * r + 1], rr[4 * r + 2], rr[4 * r + 3]);
     }
   };
-  // Bottoms j0 .. j0+nsteps-1 (j0 = 1 mod 4, nsteps = 0 mod 4, last record read
-  // j0+nsteps+1 <= h) for this warp's targets (priv row pp); `seed` is the LUT
-  // row LUT[.][j0-1].  Software-pipelined: the next pair's records and object
-  // means are computed before the current pair's table loads.
-  auto rect_run = [&](const float* seed, int j0, int nsteps, const float* pp, uint32_t Tk,
-                      uint32_t N4k, float& best, int& argj) {
-    float rr[4 * NR];
+  auto load_seed = [&](float (&rr)[4 * NR], const float* row) {
 #pragma unroll
-    for (int r = 0; r < NR; ++r) {
-      float4 x = make_float4(seed[4 * lane + 128 * r], seed[4 * lane + 128 * r + 1],
-                             seed[4 * lane + 128 * r + 2], seed[4 * lane + 128 * r + 3]);
-      rr[4 * r + 0] = x.x; rr[4 * r + 1] = x.y; rr[4 * r + 2] = x.z; rr[4 * r + 3] = x.w;
+    for (int r = 0; r < NR; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) rr[4 * r + c] = row[4 * lane + 128 * r + c];
+  };
+  // Bottoms j0 .. j0+nsteps-1 (j0 = 1 mod 4, nsteps = 0 mod 4) for this warp's
+  // targets (priv row at shared address pp_s); rr holds the W-row W[.][j0-1].
+  // Candidates are shifted by -cap*(k+1):  (P_k - W_j)[f] + min(aO', aG').
+  // Software-pipelined: the next pair's records and object means are computed
+  // before the current pair's table loads.  Shared memory is addressed with
+  // explicit 32-bit offsets.
+  const uint32_t rec_s = (uint32_t)__cvta_generic_to_shared(cs.rec);
+  const uint32_t m2_s = (uint32_t)__cvta_generic_to_shared(M2s);   // (dynamic smem does not start at 0)
+  const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ringw);
+  const uint32_t bbuf_s = ring_s + ((lane < 16) ? DP * 4 : 0) + (uint32_t)((boff - 1) * 4);
+  auto rect_run = [&](float (&rr)[4 * NR], int j0, int nsteps, uint32_t pp_s, uint32_t Tk,
+                      uint32_t N4k, float& best, int& argj) {
+    // sparse band round on the shared addresses (drp code 0 = invalid -> no-op)
+    auto band = [&](int drpA, int drpB) {
+      const int drp = (lane < 16) ? drpA : drpB;
+      const uint32_t f = (uint32_t)(drp - 1 + boff);
+      if (blive && drp != 0 && f < (uint32_t)DP) {
+        float* q = shp<float>(bbuf_s + 4u * (uint32_t)drp);
+        *q -= bwt;
+      }
+    };
+    auto rowj = [&](int j) {
+      const uint4* q = shp<const uint4>(rec_s + 32u * (uint32_t)j);
+      return unpack_row(q[0], q[1]);
+    };
+    auto cell = [&](const RowU& r, int j, int f, float pw) {
+      float aO = (f > r.ordthr) ? r.AO1 : r.AO0;
+      float aG = (f >= a.thrA1[j]) ? r.AGh : ((f < a.thrB[j]) ? r.AGl : r.AGm);
+      float cand = pw + fminf(aO, aG);
+      if (cand < best) { best = cand; argj = j; }
+    };
+    auto fmean = [&](const RowU& r) {
+      const uint32_t n4 = N4k - r.N4;
+      const uint32_t M = *shp<const uint32_t>(m2_s + n4);
+      return min((int)__umulhi((Tk - r.T) >> (kRBits - 1), M), Dm1);
+    };
+    RowU r0 = rowj(j0), r1 = rowj(j0 + 1);
+    if constexpr (SPARSE) {
+      // both buffers := W_{j0-1}; then buffer 1 = W_{j0}, buffer 0 = W_{j0+1}
+      const int drm = rowj(j0 - 1).drp;
+#pragma unroll
+      for (int r = 0; r < NR; ++r) {
+        const float4 v = make_float4(rr[4 * r], rr[4 * r + 1], rr[4 * r + 2], rr[4 * r + 3]);
+        *shp<float4>(ring_s + 16u * lane + 512u * r) = v;
+        *shp<float4>(ring_s + DP * 4u + 16u * lane + 512u * r) = v;
+      }
+      __syncwarp();
+      band(drm, drm);
+      __syncwarp();
+      band(0, r0.drp);
+    } else {
+      ring_step(rr, j0 - 1, 1);
+      ring_step(rr, j0, 2);
     }
-    ring_step(rr, j0 - 1, 1);
-    ring_step(rr, j0, 2);
-    RowU r0 = load_row_c(cs.rec, j0), r1 = load_row_c(cs.rec, j0 + 1);
-    int f0 = span_f(Tk - r0.T, N4k - r0.N4, smem, Dm1);
-    int f1 = span_f(Tk - r1.T, N4k - r1.N4, smem, Dm1);
+    int f0 = fmean(r0), f1 = fmean(r1);
+    const int jl = j0 + nsteps - 1;
     __syncwarp();
 #pragma unroll 1
     for (int jj = 0; jj < nsteps; jj += 4) {
 #pragma unroll
       for (int half = 0; half < 2; ++half) {
-        const int jA = j0 + jj + 2 * half;          // slots (jA & 3) = 1 + 2 half
-        // prefetch the next pair (rows jA+2, jA+3; static fields only matter for f)
-        // (clamped: the pair after the last one is loaded but not used)
-        const RowU n0 = load_row_c(cs.rec, min(jA + 2, h)), n1 = load_row_c(cs.rec, min(jA + 3, h));
-        const int g0 = span_f(Tk - n0.T, N4k - n0.N4, smem, Dm1);
-        const int g1 = span_f(Tk - n1.T, N4k - n1.N4, smem, Dm1);
-        const float* ra = ringw + ((1 + 2 * half) & 3) * DP;
-        const float* rb = ringw + ((2 + 2 * half) & 3) * DP;
-        {
-          float data = pp[f0] - ra[f0];
-          float aO = (f0 > r0.ordthr) ? r0.AO1 : r0.AO0;
-          float aG = (f0 >= r0.thrA1) ? r0.AGh : ((f0 < r0.thrB) ? r0.AGl : r0.AGm);
-          float cand = data + fminf(aO, aG);
-          if (cand < best) { best = cand; argj = jA; }
+        const int jA = j0 + jj + 2 * half;          // odd
+        // next pair (rows jA+2, jA+3), clamped to the run's last row jl <= k so the
+        // object-mean lookup stays in range (the pair after the last is unused)
+        const RowU n0 = rowj(min(jA + 2, jl)), n1 = rowj(min(jA + 3, jl));
+        const int g0 = fmean(n0), g1 = fmean(n1);
+        const uint32_t ra = SPARSE ? ring_s + DP * 4u : ring_s + ((1 + 2 * half) & 3) * DP * 4u;
+        const uint32_t rb = SPARSE ? ring_s : ring_s + ((2 + 2 * half) & 3) * DP * 4u;
+        const float p0 = *shp<const float>(pp_s + 4u * f0), p1 = *shp<const float>(pp_s + 4u * f1);
+        const float w0 = *shp<const float>(ra + 4u * f0), w1 = *shp<const float>(rb + 4u * f1);
+        cell(r0, jA, f0, p0 - w0);
+        cell(r1, jA + 1, f1, p1 - w1);
+        if constexpr (SPARSE) {
+          // buffer 1: W_jA -> W_{jA+2}; buffer 0: W_{jA+1} -> W_{jA+3}
+          __syncwarp();
+          band(r0.drp, r1.drp);
+          __syncwarp();
+          band(r1.drp, n0.drp);
+        } else {
+          ring_step(rr, jA + 1, (3 + 2 * half) & 3);
+          ring_step(rr, jA + 2, (4 + 2 * half) & 3);
         }
-        {
-          float data = pp[f1] - rb[f1];
-          float aO = (f1 > r1.ordthr) ? r1.AO1 : r1.AO0;
-          float aG = (f1 >= r1.thrA1) ? r1.AGh : ((f1 < r1.thrB) ? r1.AGl : r1.AGm);
-          float cand = data + fminf(aO, aG);
-          if (cand < best) { best = cand; argj = jA + 1; }
-        }
-        ring_step(rr, jA + 1, (3 + 2 * half) & 3);
-        ring_step(rr, jA + 2, (4 + 2 * half) & 3);
         r0 = n0; r1 = n1; f0 = g0; f1 = g1;
         __syncwarp();
       }
     }
   };
+  // Full 32-row chunks m < mend for this warp's targets, handed out dynamically;
+  // the anchor row of the next chunk is prefetched from L2 while one runs.
+  auto bulk_chunks = [&](int mend, uint32_t pp_s, uint32_t Tk, uint32_t N4k, float& best,
+                         int& argj) {
+    int m = 0;
+    if (lane == 0) m = atomicAdd(cs.ctr, 1);
+    m = __shfl_sync(0xffffffffu, m, 0);
+    float rr[4 * NR];
+    if (m < mend) load_seed(rr, ANg + m * DP);
+    while (m < mend) {
+      int m2 = 0;
+      if (lane == 0) m2 = atomicAdd(cs.ctr, 1);
+      m2 = __shfl_sync(0xffffffffu, m2, 0);
+      float nx[4 * NR];
+#pragma unroll
+      for (int i = 0; i < 4 * NR; ++i) nx[i] = 0.f;
+      if (m2 < mend) load_seed(nx, ANg + m2 * DP);
+      rect_run(rr, 32 * m + 1, 32, pp_s, Tk, N4k, best, argj);
+#pragma unroll
+      for (int i = 0; i < 4 * NR; ++i) rr[i] = nx[i];
+      m = m2;
+    }
+  };
 
-  float fr[NSW];                       // rectangle warps: LUT_object[f][32 bt] of their f slices
+  float fr[NSW];                       // rectangle warps: W[f][32 bt] of their f slices
 
   for (int item = slot_global; item < a.items; item += gridDim.x * a.cols_per_cta) {
     const uint16_t* col = a.cols + (int64_t)item * h;
     // ---------------- prologue A (all 4 warps): per-pixel costs (a3-a4) ----------
-    float* tG = cs.ring;                 // temporaries in the (idle) ring + cell area
-    float* tS = cs.ring + h;
-    uint32_t* tD = reinterpret_cast<uint32_t*>(cs.ring + 2 * h);
+    float* tG = cs.priv;                 // temporaries in the (idle) priv rows
+    float* tS = cs.priv + h;
+    uint32_t* tD = reinterpret_cast<uint32_t*>(cs.priv + 2 * h);
     for (int v = ctid; v < h + 2; v += kCW * 32) {
       int dR = -1;
       if (v < h) {
         uint32_t u = col[v];
         dR = (u == 0xffffu) ? -1 : (int)u;
       }
-      bool valid = dR >= 0;
+      const bool valid = dR >= 0;
+      const int dr = valid ? (dR + (1 << (kRBits - 1))) >> kRBits : -1;   // round half up (L#9)
       if (v < h) {
-        float xg = a.capQ, xs = a.capQ;
+        float xg = capQ, xs = capQ;
         if (valid) {
           xg = __ldg(a.gG + min(abs(dR - __ldg(a.dgR + v)), a.LG - 1));
           xs = __ldg(a.gS + min(dR, a.LS - 1));
         }
         tG[v] = xg; tS[v] = xs;
         tD[v] = valid ? (uint32_t)dR + (1u << (kRBits - 1)) : 0u;
-        cs.rec[2 * v + 3].w = a.thr[v + 1 < h ? v + 1 : h - 1];
       }
-      // object pixel disparity rounded half up (L#9) -> E offsets of this row
-      int dmr = valid ? a.D - ((dR + (1 << (kRBits - 1))) >> kRBits) : a.dmr_inv;
+      if (v <= h)                        // static record word of row v: pixel code (ordthr later)
+        cs.rec[2 * v + 1].w = (uint32_t)(dr + 1) << 16;
+      if (v < 2) {                       // padding rows h+1, h+2 and row 0: T = N4 = 0
+        cs.rec[2 * (h + 1 + v) + 1] = make_uint4(0, 0, 0, 0);
+        cs.rec[2 * (h + 1 + v)] = make_uint4(0, 0, 0, 0);
+        if (v == 0) { cs.rec[1].y = 0; cs.rec[1].z = 0; }
+      }
+      // E offsets of this row
+      int dmr = valid ? a.D - dr : a.dmr_inv;
       int cc = dmr & 3;
       cs.eo[v] = (uint32_t)(cc * a.esz * 4 + (dmr - cc) * 4) | ((uint32_t)(dmr * 4) << 16);
     }
-    for (int i = ctid; i < DP; i += kCW * 32) cs.anchor[i] = 0.f;   // anchor 0 = LUT[.][0] = 0
+    for (int i = ctid; i < DP; i += kCW * 32) ANg[i] = 0.f;   // W[.][0] = 0
+    if (ctid == 0) *cs.ctr = 0;
     named_bar(bar_col, kCW * 32);
 
-    // build priv rows of block bt (rectangle warps, f slices rw, rw+3, ...) and the
+    // ---------------- prologue B (4 warps): prefix sums --------------
+    // warp 0: ground PG, warp 1: sky PS, warp 2: disparity T, warp 3: count N4
+    {
+      float cf = 0.f;
+      uint32_t cu = 0;
+      if (lane == 0) { if (w == 0) PGg[0] = 0.f; if (w == 1) PSg[0] = 0.f; }
+      for (int v0 = 0; v0 < h; v0 += 32) {
+        const int v = v0 + lane;
+        if (w < 2) {
+          const float x = (v < h) ? ((w == 0) ? tG[v] : tS[v]) : 0.f;
+          const float in = warp_incl_scan(x, lane) + cf;
+          if (v < h) ((w == 0) ? PGg : PSg)[v + 1] = in;
+          cf = __shfl_sync(0xffffffffu, in, 31);
+        } else {
+          const uint32_t t = (v < h) ? tD[v] : 0u;
+          const uint32_t x = (w == 2) ? t : (t ? 4u : 0u);
+          const uint32_t in = warp_incl_scan(x, lane) + cu;
+          if (v < h) {
+            if (w == 2) cs.rec[2 * (v + 1) + 1].y = in;   // T[v+1]
+            else cs.rec[2 * (v + 1) + 1].z = in;          // N4[v+1]
+          }
+          cu = __shfl_sync(0xffffffffu, in, 31);
+        }
+      }
+      __threadfence_block();
+    }
+    named_bar(bar_col, kCW * 32);
+
+    // build priv W-rows of block bt (rectangle warps, f slices rw, rw+3, ...) and the
     // anchor row 32(bt+1): a sequential prefix over rows, per f.  The
     // row offsets come from lane registers by shuffle; loads of 8 rows are issued
     // before their prefix chain.
@@ -471,86 +606,59 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
       }
 #pragma unroll
       for (int q = 0; q < NSW; ++q)
-        if (q < nq) cs.anchor[(bt + 1) * DP + 32 * rw + 96 * q + lane] = fr[q];
+        if (q < nq) ANg[(bt + 1) * DP + 32 * rw + 96 * q + lane] = fr[q];
     };
     // triangle cells of block bt: bottom K0+1+j', target K0+k' (k' > j'); their
-    // bottoms' LUT rows are the block's own priv rows: data, f, gravity level.
-    // The 496 cells are spread densely over the 96 rectangle threads.  Also keeps
-    // the LUT rows K0+12 and K0+24 as seeds for block bt+1's newest chunk.
+    // bottoms' W-rows are the block's own priv rows: data term (absolute),
+    // f, gravity level.  The 496 cells are spread densely over the column group.
+    // Also keeps the W-rows K0+8, K0+16, K0+24 as seeds of block bt+1's newest chunk.
     auto precompute_cells = [&](int bt) {
       const int K0b = bt << 5;
       const int jn = min(K0b + 31, h - 1) - K0b;
       const int ncell = tri_off(jn);
-      for (int idx = rw * 32 + lane; idx < ncell; idx += 96) {
+      for (int idx = ctid; idx < ncell; idx += kCW * 32) {
         const uint32_t jk = tri_jk[idx];
         const int jp = jk & 0xff, kp = jk >> 8;
         const int k = K0b + kp;
         if (k < h) {
           const uint4 ry = cs.rec[2 * (K0b + jp + 1) + 1];
           const uint4 rk = cs.rec[2 * (k + 1) + 1];
-          int f = span_f(rk.y - ry.y, (rk.z & 0xffffu) - (ry.z & 0xffffu), smem, Dm1);
-          float data = cs.priv[kp * (DP + 1) + f] - cs.priv[jp * (DP + 1) + f];
-          int lvl = (f >= (int)(ry.w & 0xffffu)) ? 1 : ((f < (int)(ry.w >> 16)) ? 2 : 0);
+          int f = span_f(rk.y - ry.y, rk.z - ry.z, smem, Dm1);
+          float data = (cs.priv[kp * (DP + 1) + f] - cs.priv[jp * (DP + 1) + f]) + capQ * (float)(kp - jp);
+          const uint32_t th = __ldg(a.thrg + K0b + jp + 1);
+          int lvl = (f >= (int)(th & 0xffffu)) ? 1 : ((f < (int)(th >> 16)) ? 2 : 0);
           cs.cbd[idx] = data;
           cs.cbf[idx] = (uint16_t)(f | (lvl << 12));
         }
       }
-      if (rw < 2 && K0b + 32 < h) {     // seeds (only needed if a next block exists)
-        float* sd = cs.seed + ((bt & 1) * 2 + rw) * DP;
-        const float* row = cs.priv + (12 * rw + 11) * (DP + 1);
+      if (w > 0 && K0b + 32 < h) {      // seeds (only needed if a next block exists)
+        float* sd = cs.seed + ((bt & 1) * 3 + w - 1) * DP;
+        const float* row = cs.priv + (8 * w - 1) * (DP + 1);
         for (int f = lane; f < DP; f += 32) sd[f] = row[f];
       }
     };
 
-    // ---------------- prologue B (warp 0): prefix sums ---------------
-    // meanwhile the rectangle warps build block 0's priv rows
-    if (w == 0) {
-      float cg = 0.f, cs_ = 0.f;
-      uint32_t ct = 0, cn = 0;
-      if (lane == 0) { PGg[0] = 0.f; PSg[0] = 0.f; }
-      for (int v0 = 0; v0 < h; v0 += 32) {
-        int v = v0 + lane;
-        float xg = 0.f, xs = 0.f;
-        uint32_t xt = 0, xn = 0;
-        if (v < h) {
-          xg = tG[v]; xs = tS[v]; xt = tD[v]; xn = xt ? 4u : 0u;
-        }
-        float ig = warp_incl_scan(xg, lane) + cg;
-        float is = warp_incl_scan(xs, lane) + cs_;
-        uint32_t it = warp_incl_scan(xt, lane) + ct;
-        uint32_t in = warp_incl_scan(xn, lane) + cn;
-        if (v < h) {
-          PGg[v + 1] = ig; PSg[v + 1] = is;
-          cs.rec[2 * (v + 1) + 1].y = it;            // T[v+1]
-          cs.rec[2 * (v + 1) + 1].z = in;            // N4[v+1]
-        }
-        cg = __shfl_sync(0xffffffffu, ig, 31);
-        cs_ = __shfl_sync(0xffffffffu, is, 31);
-        ct = __shfl_sync(0xffffffffu, it, 31);
-        cn = __shfl_sync(0xffffffffu, in, 31);
-      }
-      __threadfence_block();
-    } else {
+    if (w != 0) {
 #pragma unroll
       for (int q = 0; q < NSW; ++q) fr[q] = 0.f;
       build_priv(0);
     }
     named_bar(bar_col, kCW * 32);
 
-    // rectangle warps: block 0 has only the j = 0 candidate (Eq. 5) and its triangle
-    float rbest = INF;
-    int rargj = 0x7fffffff;
-    if (w != 0) {
+    // block 0 has only the j = 0 candidate (Eq. 5) and its triangle
+    {
       const int kk = lane < h ? lane : h - 1;
       const uint4 rky = cs.rec[2 * (kk + 1) + 1];
-      const uint32_t Tk = rky.y, N4k = rky.z & 0xffffu;
+      const uint32_t Tk = rky.y, N4k = rky.z;
       const float* pp = cs.priv + lane * (DP + 1);
-      if (rw == 0) {
+      float rbest = INF;
+      int rargj = 0x7fffffff;
+      if (w == 1) {
         int f = span_f(Tk, N4k, smem, Dm1);
-        rbest = pp[f] + a.piFirstO;
+        rbest = pp[f] + a.piFirstO;      // shifted by -cap*(k+1)
         rargj = 0;
       }
-      cs.part[rw * 32 + lane] = make_float2(rbest, __int_as_float(rargj));
+      cs.part[w * 32 + lane] = make_float2(rbest, __int_as_float(rargj));
       precompute_cells(0);
     }
     named_bar(bar_col, kCW * 32);
@@ -564,21 +672,25 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
     for (int b = 0; b < nb; ++b) {
       const int K0 = b << 5;
       const int k = K0 + lane;
+      const int bn = b + 1;
+      const int Kn = bn << 5;
+      const bool has_next = bn < nb;
       if (w == 0) {
         // ============ serial warp: block b's triangle and finalisation ============
         const int kk = k < h ? k : h - 1;
         const uint4 rky = cs.rec[2 * (kk + 1) + 1];
-        const uint32_t N4k = rky.z & 0xffffu;
+        const uint32_t N4k = rky.z;
         const uint32_t Tk = rky.y;
         const float pg0 = PGg[kk], pg1 = PGg[kk + 1], ps0 = PSg[kk], ps1 = PSg[kk + 1];
         float best = INF;
         int argj = 0x7fffffff;
 #pragma unroll
-        for (int q = 0; q < 3; ++q) {
+        for (int q = 0; q < kCW; ++q) {
           float2 p = cs.part[q * 32 + lane];
           int pj = __float_as_int(p.y);
           if (p.x < best || (p.x == best && pj < argj)) { best = p.x; argj = pj; }
         }
+        best += capQ * (float)(k + 1);   // undo the rectangle's per-target shift
         // f and c' of the winner (the rectangle tracked only its j); packed
         // index-table entry: j | c' << 12 | f << 14
         int argf, argc;
@@ -588,8 +700,9 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
         } else {
           const RowU r = load_row(cs.rec, argj);
           argf = span_f(Tk - r.T, N4k - r.N4, smem, Dm1);
+          const uint32_t th = __ldg(a.thrg + argj);
           float aO = (argf > r.ordthr) ? r.AO1 : r.AO0;
-          float aG = (argf >= r.thrA1) ? r.AGh : ((argf < r.thrB) ? r.AGl : r.AGm);
+          float aG = (argf >= (int)(th & 0xffffu)) ? r.AGh : ((argf < (int)(th >> 16)) ? r.AGl : r.AGm);
           argc = (aG <= aO) ? 0 : 1;
         }
         int pack = argj | (argc << 12) | (argf << 14);
@@ -665,52 +778,55 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
           off += 31 - jp;
         }
         // every lane now holds the final values of its target row k: write the
-        // record of row k+1 (consumed by later rectangles) and the index table
+        // record of row k+1 (consumed by later rectangles; predecessor terms
+        // shifted by -cap*(k+1)) and the index table
         if (k < h) {
           const int af = pack >> 14;
-          cs.rec[2 * (k + 1)] = make_uint4(__float_as_uint(best + a.kOO_lo), __float_as_uint(best + a.kOO_hi),
-                                           __float_as_uint(myCG + a.kGO_mid), __float_as_uint(myCG + a.kGO_hi));
+          const float sh = capQ * (float)(k + 1);
+          cs.rec[2 * (k + 1)] = make_uint4(__float_as_uint((best + a.kOO_lo) - sh), __float_as_uint((best + a.kOO_hi) - sh),
+                                           __float_as_uint((myCG + a.kGO_mid) - sh), __float_as_uint((myCG + a.kGO_hi) - sh));
           uint32_t* ry = reinterpret_cast<uint32_t*>(cs.rec + 2 * (k + 1) + 1);
-          ry[0] = __float_as_uint(myCG + a.kGO_lo);
-          ry[2] = N4k | ((uint32_t)(af + a.ord_margin) << 16);
+          ry[0] = __float_as_uint((myCG + a.kGO_lo) - sh);
+          ry[3] = (rky.w & 0xffff0000u) | (uint32_t)(af + a.ord_margin);
           cs.argO[k] = (uint16_t)(pack & 0x3fff);
           cs.argG[k] = (uint16_t)myG;
           cs.argS[k] = (uint16_t)myS;
           cs.fpv[k] = (uint8_t)af;
         }
-      }
-      // ======== rectangle warps: block b+1, bottoms final before block b ========
-      const int bn = b + 1;
-      const int Kn = bn << 5;
-      const bool has_next = bn < nb;
-      uint32_t Tn = 0, N4n = 0;
-      const float* ppn = cs.priv + lane * (DP + 1);
-      if (w != 0 && has_next) {
+        if (has_next) named_bar(bar_x, kCW * 32);   // block b+1's priv rows are ready
+      } else if (has_next) {
         build_priv(bn);                  // block b's priv rows are no longer needed
         named_bar(bar_rect, 3 * 32);
+        asm volatile("bar.arrive %0, %1;" ::"r"(bar_x), "r"(kCW * 32) : "memory");
+      }
+      // ======== all warps: block b+1, bottoms final before block b ===============
+      float rbest = INF;
+      int rargj = 0x7fffffff;
+      uint32_t Tn = 0, N4n = 0;
+      const float* ppn = cs.priv + lane * (DP + 1);
+      const uint32_t ppn_s = (uint32_t)__cvta_generic_to_shared(ppn);
+      if (has_next) {
         const int kk = Kn + lane < h ? Kn + lane : h - 1;
         const uint4 rky = cs.rec[2 * (kk + 1) + 1];
-        Tn = rky.y; N4n = rky.z & 0xffffu;
-        rbest = INF; rargj = 0x7fffffff;
-        if (rw == 0) {                 // j = 0: first stixel spans 0..k (Eq. 5)
+        Tn = rky.y; N4n = rky.z;
+        if (w == 1) {                  // j = 0: first stixel spans 0..k (Eq. 5)
           int f = span_f(Tn, N4n, smem, Dm1);
           rbest = ppn[f] + a.piFirstO;
           rargj = 0;
         }
         // full chunks m <= b-1: their records (rows <= 32 b) were final before block b
-        for (int m = rw; m <= b - 1; m += 3)
-          rect_run(cs.anchor + m * DP, 32 * m + 1, 32, ppn, Tn, N4n, rbest, rargj);
+        bulk_chunks(b, ppn_s, Tn, N4n, rbest, rargj);
       }
       named_bar(bar_col, kCW * 32);
-      if (w != 0 && has_next) {
+      if (has_next) {
         // newest chunk (bottoms K0+1 .. K0+32, final after block b's triangle),
-        // split 12 / 12 / 8 rows, seeded from LUT rows K0, K0+12, K0+24
-        const int j0 = K0 + 1 + 12 * rw;
-        const int ns = (rw == 2) ? 8 : 12;
-        const float* seed = (rw == 0) ? cs.anchor + b * DP : cs.seed + ((b & 1) * 2 + rw - 1) * DP;
-        rect_run(seed, j0, ns, ppn, Tn, N4n, rbest, rargj);
-        cs.part[rw * 32 + lane] = make_float2(rbest, __int_as_float(rargj));
+        // 8 rows per warp, seeded from W-rows K0, K0+8, K0+16, K0+24
+        float rr[4 * NR];
+        load_seed(rr, (w == 0) ? ANg + b * DP : cs.seed + ((b & 1) * 3 + w - 1) * DP);
+        rect_run(rr, K0 + 1 + 8 * w, 8, ppn_s, Tn, N4n, rbest, rargj);
+        cs.part[w * 32 + lane] = make_float2(rbest, __int_as_float(rargj));
         precompute_cells(bn);
+        if (ctid == 0) *cs.ctr = 0;
       }
       named_bar(bar_col, kCW * 32);
     }
