@@ -62,10 +62,31 @@ def params_dict():
     return mp.make()
 
 
+def frame_indices(rank, n):
+    """Seeded frame indices of a rank's pool (config 3 = C3): disjoint per rank,
+    since frames are sharded (weak scaling, each rank owns its own batch)."""
+    return [rank * 100000 + i for i in range(n)]
+
+
 def frame_pool(n, rank):
     from inputs import synth
-    # config id 3 (C3); each rank draws its own frames (weak scaling)
-    return np.stack([synth.frame(3, rank * 100000 + i, W_IMG, H_IMG, D_MAX) for i in range(n)])
+    return np.stack([synth.frame(3, i, W_IMG, H_IMG, D_MAX) for i in frame_indices(rank, n)])
+
+
+def max_over_ranks(value, world, device=None):
+    """Max of a per-rank time over all ranks (the job ends when the slowest rank
+    does); a no-op at world size 1."""
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def aggregate_value(frames_per_rank, steps, world, max_ms):
+    """Whole-job throughput: frames of all ranks / slowest rank's time."""
+    return frames_per_rank * world * steps / (max_ms / 1000.0)
 
 
 def cells_per_frame():
@@ -276,12 +297,9 @@ def main():
     dp = [e[1].elapsed_time(e[2]) for e in evs]
     step_ms = [r + d for r, d in zip(red, dp)]
     total_ms = sum(step_ms)
-    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    max_ms = float(t.item())
+    max_ms = max_over_ranks(total_ms, world, dev)
     frames_total = B * world * args.steps
-    value = frames_total / (max_ms / 1000.0)
+    value = aggregate_value(B, args.steps, world, max_ms)
 
     # roofline of the dominant kernel (the DP): algorithmic ALU ops / duration
     peaks = measured_peaks()
@@ -323,10 +341,8 @@ def main():
         for _ in range(e_steps):
             hd2.compute_host_ptr(hin.data_ptr(), pitch, eb, hout.data_ptr(), hcnt.data_ptr(),
                                  hcost.data_ptr())
-        dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(dt, op=dist.ReduceOp.MAX)
-        e2e = {"value": world * eb * e_steps / float(dt.item()), "unit": "frames/s",
+        dt = max_over_ranks(time.perf_counter() - t0, world, dev)
+        e2e = {"value": world * eb * e_steps / dt, "unit": "frames/s",
                "h2d_bytes_per_step": eb * H_IMG * pitch,
                "d2h_bytes_per_step": eb * hd2.n_cols * (hd2.cap * 12 + 8),
                "frames_per_step": eb, "max_stixels": 128,
