@@ -16,6 +16,7 @@
 // exact and decisions match the double-precision oracle bit for bit.
 #pragma once
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 #include "../../include/stixels.h"
@@ -581,32 +582,39 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
       const int K0b = bt << 5;
       const int rows = min(32, h - K0b);
       const uint32_t eor = cs.eo[K0b + min(lane, rows - 1)] >> 16;
-      const int nq = (NS - rw + 2) / 3;            // slices of this warp (warp-uniform)
-      for (int i0 = 0; i0 < rows; i0 += 8) {
-        float x[8][NSW];
+      const uint32_t dst_s = (uint32_t)__cvta_generic_to_shared(cs.priv) + (32 * rw + lane) * 4;
+      const uint32_t src_s = (uint32_t)__cvta_generic_to_shared(E) + (32 * rw + lane) * 4;
+      auto run = [&](auto nqc) {
+        constexpr int nq = decltype(nqc)::value;     // slices of this warp
 #pragma unroll
-        for (int r = 0; r < 8; ++r) {
-          const uint32_t e = __shfl_sync(0xffffffffu, eor, (i0 + r) & 31);
-          const float* src = reinterpret_cast<const float*>(Eb + e) + 32 * rw + lane;
+        for (int i0 = 0; i0 < 32; i0 += 8) {
+          if (i0 < rows) {
+            float x[8][nq];
 #pragma unroll
-          for (int q = 0; q < NSW; ++q) x[r][q] = (q < nq) ? src[96 * q] : 0.f;
-        }
-        const int rn = min(8, rows - i0);
+            for (int r = 0; r < 8; ++r) {
+              const uint32_t e = __shfl_sync(0xffffffffu, eor, i0 + r);
 #pragma unroll
-        for (int r = 0; r < 8; ++r) {
-          if (r < rn) {
-            float* dst = cs.priv + (i0 + r) * (DP + 1) + 32 * rw + lane;
+              for (int q = 0; q < nq; ++q) x[r][q] = *shp<const float>(src_s + e + 384u * q);
+            }
 #pragma unroll
-            for (int q = 0; q < NSW; ++q) {
-              fr[q] += x[r][q];
-              if (q < nq) dst[96 * q] = fr[q];
+            for (int r = 0; r < 8; ++r) {
+              if (i0 + r < rows) {
+#pragma unroll
+                for (int q = 0; q < nq; ++q) {
+                  fr[q] += x[r][q];
+                  *shp<float>(dst_s + ((i0 + r) * (DP + 1) + 96 * q) * 4u) = fr[q];
+                }
+              }
             }
           }
         }
-      }
 #pragma unroll
-      for (int q = 0; q < NSW; ++q)
-        if (q < nq) ANg[(bt + 1) * DP + 32 * rw + 96 * q + lane] = fr[q];
+        for (int q = 0; q < nq; ++q) ANg[(bt + 1) * DP + 32 * rw + 96 * q + lane] = fr[q];
+      };
+      const int nq = (NS - rw + 2) / 3;
+      if (nq == 1) run(std::integral_constant<int, 1>());
+      else if (nq == 2) run(std::integral_constant<int, (NSW >= 2 ? 2 : 1)>());
+      else run(std::integral_constant<int, NSW>());
     };
     // triangle cells of block bt: bottom K0+1+j', target K0+k' (k' > j'); their
     // bottoms' W-rows are the block's own priv rows: data term (absolute),
@@ -663,11 +671,12 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
     }
     named_bar(bar_col, kCW * 32);
 
-    // serial-warp state: running minima of ground / sky (warp-uniform), last C values
-    float MG = a.piFirstG, MS = INF;
-    int gj = 0, sj = 0, sc = kStart;
-    float prevCO = INF, prevCG = INF, lastO = INF, lastG = INF, lastS = INF;
-    int prevF = 0;
+    // serial-warp state carried across blocks (warp-uniform): last row's C values,
+    // ground / sky running minima (value, argmin) of Eq. 6's G and S rows
+    float cCO = INF, cCG = INF;          // C_O[K0-1], C_G[K0-1]
+    float MG = a.piFirstG, MS = INF;     // min over bottoms j of (C[j-1] + t - P[j]), j=0 first
+    int gj = 0, sj = 0;                  // argmin (j | c' << 12 for sky)
+    float lastO = INF, lastG = INF, lastS = INF;
 
     for (int b = 0; b < nb; ++b) {
       const int K0 = b << 5;
@@ -691,8 +700,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
           if (p.x < best || (p.x == best && pj < argj)) { best = p.x; argj = pj; }
         }
         best += capQ * (float)(k + 1);   // undo the rectangle's per-target shift
-        // f and c' of the winner (the rectangle tracked only its j); packed
-        // index-table entry: j | c' << 12 | f << 14
+        // f and c' of the winner (the rectangle tracked only its j)
         int argf, argc;
         if (argj == 0) {
           argf = span_f(Tk, N4k, smem, Dm1);
@@ -705,44 +713,25 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
           float aG = (argf >= (int)(th & 0xffffu)) ? r.AGh : ((argf < (int)(th >> 16)) ? r.AGl : r.AGm);
           argc = (aG <= aO) ? 0 : 1;
         }
-        int pack = argj | (argc << 12) | (argf << 14);
-        cs.pgps[lane] = make_float4(pg0, pg1, ps0, ps1);
+        const float kOG = a.kOG;
+        // per row j = K0 + lane: {kOG - PG[j], PG[j+1]} for the in-loop ground chain
+        cs.pgps[lane] = make_float4(kOG - pg0, pg1, 0.f, 0.f);
         __syncwarp();
         const float oh = opaque(a.kOO_hi), ol = opaque(a.kOO_lo);
         const float gh = opaque(a.kGO_hi), gl = opaque(a.kGO_lo), gm = opaque(a.kGO_mid);
         const int om = a.ord_margin;
 
-        float myCG = 0.f;
-        int myG = 0, myS = 0;
-        // ground / sky running minima for target kf from C[kf-1] (warp-uniform)
-        auto ground_sky = [&](int kf, float4 q) {
-          if (kf == 0) {
-            MG = a.piFirstG; gj = 0; MS = INF; sj = 0; sc = kStart;
-          } else {
-            float vG = prevCO + a.kOG - q.x;
-            if (vG < MG) { MG = vG; gj = kf; }
-            float v1 = prevCG + a.kGS - q.z;
-            if (v1 < MS) { MS = v1; sj = kf; sc = 0; }
-            float v2 = prevCO + a.kOS - q.z;
-            if (v2 < MS) { MS = v2; sj = kf; sc = 1; }
-          }
-          float CGk = q.y + MG, CSk = q.w + MS;
-          if (lane == kf - K0) { myCG = CGk; myG = gj; myS = sj | (sc << 12); }
-          if (kf == h - 1) { lastG = CGk; lastS = CSk; }
-          return CGk;
-        };
-
-        {  // target K0: all its bottoms were in the rectangle
-          float COk = __shfl_sync(0xffffffffu, best, 0);
-          int pk = __shfl_sync(0xffffffffu, pack, 0);
-          float CGk = ground_sky(K0, cs.pgps[0]);
-          prevCO = COk; prevCG = CGk; prevF = pk >> 14;
-          if (K0 == h - 1) lastO = COk;
-        }
+        // Chain state: C_O, C_G and the object mean of the last finalised target.
+        // Target K0: all its bottoms were in the rectangle.
+        float mg = (K0 == 0) ? a.piFirstG : fminf(MG, cCO + (kOG - pg0));   // lane 0's value
+        mg = __shfl_sync(0xffffffffu, mg, 0);
+        float prevCG = __shfl_sync(0xffffffffu, pg1, 0) + mg;
+        float prevCO = __shfl_sync(0xffffffffu, best, 0);
+        int prevF = __shfl_sync(0xffffffffu, argf, 0);
         const int jn = min(K0 + 31, h - 1) - K0;
         // running minimum (over bottoms < j) of the next target to finalise
         float rB = __shfl_sync(0xffffffffu, best, 1);
-        int rP = __shfl_sync(0xffffffffu, pack, 1);
+        int rF = __shfl_sync(0xffffffffu, argf, 1);
         int off = 0;                                    // tri_off(jp)
         for (int jp = 0; jp < jn; ++jp) {
           const int j = K0 + jp + 1;                    // bottom j; target j finalised
@@ -753,14 +742,13 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
           const int df = dfl & 0xfff, dl = dfl >> 12;
           const float daO = prevCO + ((df > prevF + om) ? oh : ol);
           const float daG = prevCG + pen3(dl, gm, gh, gl);
-          const bool dpg = daG <= daO;
-          const float dc = dd + (dpg ? daG : daO);
+          const float dc = dd + fminf(daO, daG);
           const bool take = dc < rB;
           const float COj = take ? dc : rB;
-          const int Pj = take ? (j | ((dpg ? 0 : 1) << 12) | (df << 14)) : rP;
+          const int Fj = take ? df : rF;
           // this lane's cell (bottom j, target k > j) with the same predecessors
-          if (lane > jp) {
-            const int idx = off + lane - jp - 1;
+          {
+            const int idx = off + lane - jp - 1;        // (lanes <= jp read a dead slot)
             const float data = cs.cbd[idx];
             const int fl = cs.cbf[idx];
             const int f = fl & 0xfff, lvl = fl >> 12;
@@ -768,30 +756,74 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
             const float aG = prevCG + pen3(lvl, gm, gh, gl);
             const bool pg = aG <= aO;
             const float cand = data + (pg ? aG : aO);
-            if (cand < best) { best = cand; pack = j | ((pg ? 0 : 1) << 12) | (f << 14); }
+            const bool upd = (lane > jp) && (cand < best);
+            best = upd ? cand : best;
+            argj = upd ? j : argj;
+            argf = upd ? f : argf;
+            argc = upd ? (pg ? 0 : 1) : argc;
           }
           rB = __shfl_sync(0xffffffffu, best, (jp + 2) & 31);
-          rP = __shfl_sync(0xffffffffu, pack, (jp + 2) & 31);
-          const float CGj = ground_sky(j, q);
-          prevCO = COj; prevCG = CGj; prevF = Pj >> 14;
-          if (j == h - 1) lastO = COj;
+          rF = __shfl_sync(0xffffffffu, argf, (jp + 2) & 31);
+          // ground: GR^j = PG[j+1] + min(.., C_O[j-1] + t - PG[j])  (value only)
+          mg = fminf(mg, prevCO + q.x);
+          prevCG = q.y + mg;
+          prevCO = COj;
+          prevF = Fj;
           off += 31 - jp;
+        }
+        // ---- ground / sky argmins and values of the block's rows, as warp scans ----
+        // lane l = row j = K0 + l = target k: candidates at bottom j use C[j-1]
+        const float up_best = __shfl_up_sync(0xffffffffu, best, 1);     // all lanes shuffle
+        const float COm1 = (lane == 0) ? cCO : up_best;
+        float vG = (K0 == 0 && lane == 0) ? a.piFirstG : COm1 + (kOG - pg0);
+        int aG = (K0 == 0 && lane == 0) ? 0 : k;
+        if (k >= h) { vG = INF; aG = 0x7fffffff; }
+        // inclusive prefix min over lanes, ties -> lower lane (first j); carry first
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const float v2 = __shfl_up_sync(0xffffffffu, vG, o);
+          const int a2 = __shfl_up_sync(0xffffffffu, aG, o);
+          if (lane >= o && !(vG < v2)) { vG = v2; aG = a2; }
+        }
+        if (K0 > 0 && !(vG < MG)) { vG = MG; aG = gj; }
+        const float CGk = pg1 + vG;
+        const float up_cg = __shfl_up_sync(0xffffffffu, CGk, 1);
+        const float CGm1 = (lane == 0) ? cCG : up_cg;
+        float v1 = CGm1 + a.kGS - ps0, v2 = COm1 + a.kOS - ps0;    // pred G, pred O
+        float vS = (v2 < v1) ? v2 : v1;
+        int aS = (v2 < v1) ? (k | (1 << 12)) : k;
+        if ((K0 == 0 && lane == 0) || k >= h) { vS = INF; aS = (K0 == 0 && lane == 0) ? (kStart << 12) : 0x7fffffff; }
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const float v3 = __shfl_up_sync(0xffffffffu, vS, o);
+          const int a3 = __shfl_up_sync(0xffffffffu, aS, o);
+          if (lane >= o && !(vS < v3)) { vS = v3; aS = a3; }
+        }
+        if (K0 > 0 && !(vS < MS)) { vS = MS; aS = sj; }
+        const float CSk = ps1 + vS;
+        // carry to the next block: last row of this block (lane 31, or h-1)
+        const int L = min(31, h - 1 - K0);
+        MG = __shfl_sync(0xffffffffu, vG, L); gj = __shfl_sync(0xffffffffu, aG, L);
+        MS = __shfl_sync(0xffffffffu, vS, L); sj = __shfl_sync(0xffffffffu, aS, L);
+        cCO = __shfl_sync(0xffffffffu, best, L);
+        cCG = __shfl_sync(0xffffffffu, CGk, L);
+        if (K0 + 31 >= h - 1) {
+          lastO = cCO; lastG = cCG; lastS = __shfl_sync(0xffffffffu, CSk, L);
         }
         // every lane now holds the final values of its target row k: write the
         // record of row k+1 (consumed by later rectangles; predecessor terms
         // shifted by -cap*(k+1)) and the index table
         if (k < h) {
-          const int af = pack >> 14;
           const float sh = capQ * (float)(k + 1);
           cs.rec[2 * (k + 1)] = make_uint4(__float_as_uint((best + a.kOO_lo) - sh), __float_as_uint((best + a.kOO_hi) - sh),
-                                           __float_as_uint((myCG + a.kGO_mid) - sh), __float_as_uint((myCG + a.kGO_hi) - sh));
+                                           __float_as_uint((CGk + a.kGO_mid) - sh), __float_as_uint((CGk + a.kGO_hi) - sh));
           uint32_t* ry = reinterpret_cast<uint32_t*>(cs.rec + 2 * (k + 1) + 1);
-          ry[0] = __float_as_uint((myCG + a.kGO_lo) - sh);
-          ry[3] = (rky.w & 0xffff0000u) | (uint32_t)(af + a.ord_margin);
-          cs.argO[k] = (uint16_t)(pack & 0x3fff);
-          cs.argG[k] = (uint16_t)myG;
-          cs.argS[k] = (uint16_t)myS;
-          cs.fpv[k] = (uint8_t)af;
+          ry[0] = __float_as_uint((CGk + a.kGO_lo) - sh);
+          ry[3] = (rky.w & 0xffff0000u) | (uint32_t)(argf + a.ord_margin);
+          cs.argO[k] = (uint16_t)(argj | (argc << 12));
+          cs.argG[k] = (uint16_t)aG;
+          cs.argS[k] = (uint16_t)aS;
+          cs.fpv[k] = (uint8_t)argf;
         }
         if (has_next) named_bar(bar_x, kCW * 32);   // block b+1's priv rows are ready
       } else if (has_next) {
