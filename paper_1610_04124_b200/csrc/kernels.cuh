@@ -148,10 +148,11 @@ struct DPArgs {
 struct ColSmem {
   float* priv;      // [32][DP+1]     priv[i][f] = LUT_object[f][32b+i+1] of the block being built
   float* seed;      // [2][3][DP]     LUT rows 32b+8, +16, +24 of block b (parity b & 1)
-  float* ring;      // [4][RR][DP]    per-warp W-rows W_j = LUT_object[.][j] - cap*j (RR = 2 sparse, 4 dense)
+  float* ring;      // [4][ring_stride] per-warp W-rows W_j = LUT_object[.][j] - cap*j (RR = 2 sparse, 4 dense)
   float* cbd;       // [496]          triangle cells (bottom K0+1+j', target K0+k' > j'), packed
   uint16_t* cbf;    // [496]          ... f | gravity level << 12
   uint4* rec;       // [h+3][2]       row j: {AO0,AO1,AGm,AGh} {AGl, T[j], N4[j], ordthr | drp<<16}
+  uint2* tn;        // [h+1]          row j: {T[j], N4[j]} (compact copy for per-lane rows)
   uint32_t* eo;     // [h+2]          lo16: ring window byte offset; hi16: E0 byte offset
   uint16_t* argO;   // [h]            j | c'<<12
   uint16_t* argG;   // [h]            j (pred class O, or start if j == 0)
@@ -167,15 +168,23 @@ __host__ __device__ constexpr int tri_off(int jp) { return 31 * jp - (jp * (jp -
 
 __host__ __device__ inline int al16(int x) { return (x + 15) & ~15; }
 
+// Floats of W-row ring per warp.  Sparse mode: buffer 0 at 0, buffer 1 at DP + 16,
+// so the two half-warps of a band round (one per buffer, nearly equal f) fall in
+// disjoint banks.
+template <int DP, bool SPARSE>
+__host__ __device__ constexpr int ring_stride() { return SPARSE ? 2 * DP + 16 : 4 * DP; }
+template <int DP, bool SPARSE>
+__host__ __device__ constexpr uint32_t ring_b1() { return (DP + 16) * 4u; }
+
 template <int DP, bool SPARSE>
 __host__ __device__ inline int col_smem_bytes(int h) {
-  constexpr int RR = SPARSE ? 2 : 4;
   int b = 0;
   b += al16(32 * (DP + 1) * 4);
   b += al16(6 * DP * 4);
-  b += al16(kCW * RR * DP * 4);
+  b += al16(kCW * ring_stride<DP, SPARSE>() * 4);
   b += al16(kTri * 4) + al16(kTri * 2);
   b += al16((h + 3) * 32);
+  b += al16((h + 1) * 8);
   b += al16((h + 2) * 4);
   b += al16(h * 2) * 3;
   b += al16(h);
@@ -192,14 +201,14 @@ __host__ __device__ inline int64_t col_scratch_floats(int h) {
 
 template <int DP, bool SPARSE>
 __device__ inline ColSmem carve(uint8_t* p, int h) {
-  constexpr int RR = SPARSE ? 2 : 4;
   ColSmem w;
   w.priv = reinterpret_cast<float*>(p); p += al16(32 * (DP + 1) * 4);
   w.seed = reinterpret_cast<float*>(p); p += al16(6 * DP * 4);
-  w.ring = reinterpret_cast<float*>(p); p += al16(kCW * RR * DP * 4);
+  w.ring = reinterpret_cast<float*>(p); p += al16(kCW * ring_stride<DP, SPARSE>() * 4);
   w.cbd = reinterpret_cast<float*>(p); p += al16(kTri * 4);
   w.cbf = reinterpret_cast<uint16_t*>(p); p += al16(kTri * 2);
   w.rec = reinterpret_cast<uint4*>(p); p += al16((h + 3) * 32);
+  w.tn = reinterpret_cast<uint2*>(p); p += al16((h + 1) * 8);
   w.eo = reinterpret_cast<uint32_t*>(p); p += al16((h + 2) * 4);
   w.argO = reinterpret_cast<uint16_t*>(p); p += al16(h * 2);
   w.argG = reinterpret_cast<uint16_t*>(p); p += al16(h * 2);
@@ -247,13 +256,16 @@ __device__ __forceinline__ void named_bar(int id, int threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
 
+constexpr int kNoBand = 0x4000;     // drp code of an invalid pixel (band update no-op)
+constexpr int kM2Pad = 16;          // bytes of shared memory before the M2 table
+
 // Object model value f of span [j, k] from prefix differences:
 // f = floor(t / (256 n)), t = sum(d + 128) over valid pixels: the exact half-up
 // rounded mean (L#10), via a multiply-high by ceil(2^31/n) (exact for t < 2^28),
-// clamped to D-1.  n4 = 4n is the byte offset into M2 (at the start of dynamic smem).
+// clamped to D-1.  n4 = 4n is the byte offset into M2 (kM2Pad bytes into dynamic smem).
 __device__ __forceinline__ int span_f(uint32_t t, uint32_t n4, const uint8_t* smem0, int Dm1) {
   uint32_t y = t >> (kRBits - 1);
-  uint32_t M = *reinterpret_cast<const uint32_t*>(smem0 + n4);
+  uint32_t M = *reinterpret_cast<const uint32_t*>(smem0 + kM2Pad + n4);
   return min((int)__umulhi(y, M), Dm1);
 }
 
@@ -273,7 +285,7 @@ __device__ __forceinline__ float ldsf(uint32_t addr) {
 struct RowU {
   float AO0, AO1, AGm, AGh, AGl;   // predecessor terms of row j, shifted by -cap*j
   uint32_t T, N4;
-  int ordthr, drp;                 // drp = round(d_j) + 1, 0 if pixel j is invalid
+  int ordthr, drp;                 // drp = round(d_j) + 1, kNoBand if pixel j is invalid
 };
 __device__ __forceinline__ RowU unpack_row(uint4 x, uint4 y) {
   RowU u;
@@ -320,8 +332,6 @@ template <int DP, bool SPARSE>
 __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_constant__ DPArgs a) {
   constexpr int NR = DP / 128;         // LDS.128 ring windows per lane
   constexpr int NS = DP / 32;          // 32-wide f slices
-  constexpr int NSW = (NS + 2) / 3;    // f slices per rectangle warp (at most)
-  constexpr int RR = SPARSE ? 2 : 4;   // W-rows per warp
   extern __shared__ __align__(16) uint8_t smem[];
   const int lane = threadIdx.x & 31;
   const int wid = threadIdx.x >> 5;
@@ -337,7 +347,6 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
   } else {
     cslot = wid % C; w = 1 + wid / C;
   }
-  const int rw = w - 1;                // rectangle warp index 0..2, -1 for the serial warp
   const int ctid = w * 32 + lane;      // thread index within the column group
   const int h = a.h;
   const int Dm1 = a.D - 1;
@@ -350,9 +359,11 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
   // CTA-shared tables: M2 at offset 0, then 4 shifted copies of the object
   // pair-cost window E' (Pair[f][d] - cap = E'[f - d + D]), then the
   // triangle cell decode table.
-  uint32_t* M2s = reinterpret_cast<uint32_t*>(smem);
-  float* E = reinterpret_cast<float*>(smem + al16((h + 1) * 4));
-  uint16_t* tri_jk = reinterpret_cast<uint16_t*>(smem + al16((h + 1) * 4) + 4 * a.esz * 4);
+  // M2 sits kM2Pad bytes in: the rectangle's look-ahead rows may read up to 8
+  // bytes before it (their value is never used)
+  uint32_t* M2s = reinterpret_cast<uint32_t*>(smem + kM2Pad);
+  float* E = reinterpret_cast<float*>(smem + kM2Pad + al16((h + 1) * 4));
+  uint16_t* tri_jk = reinterpret_cast<uint16_t*>(smem + kM2Pad + al16((h + 1) * 4) + 4 * a.esz * 4);
   for (int i = threadIdx.x; i <= h; i += blockDim.x) M2s[i] = a.M2[i];
   for (int i = threadIdx.x; i < 4 * a.esz; i += blockDim.x) E[i] = a.E[i];
   for (int jp = 0; jp < 31; ++jp)                 // triangle cell index -> (j', k')
@@ -362,7 +373,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
   const uint8_t* Eb = reinterpret_cast<const uint8_t*>(E);
 
   ColSmem cs = carve<DP, SPARSE>(smem + a.shared_bytes + cslot * a.col_bytes, h);
-  float* ringw = cs.ring + w * RR * DP;
+  float* ringw = cs.ring + w * ring_stride<DP, SPARSE>();
   const float INF = __int_as_float(0x7f800000);
   const int slot_global = blockIdx.x * a.cols_per_cta + cslot;
   float* PGg = a.scratch + (int64_t)slot_global * col_scratch_floats<DP>(h);
@@ -374,7 +385,8 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
   // the band and its weight cap - Pair(d)
   const int boff = (lane & 15) - 7;
   const float bwt = a.wt[lane & 15];
-  const bool blive = (lane & 15) < 15 && bwt != 0.f;
+  // dead lanes (lane 15/31, zero weight) get an offset that puts every f out of range
+  const int boffc = ((lane & 15) < 15 && bwt != 0.f) ? boff - 1 : -0x1000;
   // ---- helpers --------------------------------------------------------------
   // dense W-row step: rr += E'[.][d_src] for f = 4*lane.. (+128 r); store to slot
   auto ring_step = [&](float (&rr)[4 * NR], int row_src, int slot) {
@@ -403,14 +415,14 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
   const uint32_t rec_s = (uint32_t)__cvta_generic_to_shared(cs.rec);
   const uint32_t m2_s = (uint32_t)__cvta_generic_to_shared(M2s);   // (dynamic smem does not start at 0)
   const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ringw);
-  const uint32_t bbuf_s = ring_s + ((lane < 16) ? DP * 4 : 0) + (uint32_t)((boff - 1) * 4);
+  const uint32_t bbuf_s = ring_s + ((lane < 16) ? ring_b1<DP, SPARSE>() : 0u) + (uint32_t)((boff - 1) * 4);
   auto rect_run = [&](float (&rr)[4 * NR], int j0, int nsteps, uint32_t pp_s, uint32_t Tk,
                       uint32_t N4k, float& best, int& argj) {
-    // sparse band round on the shared addresses (drp code 0 = invalid -> no-op)
+    // sparse band round on the shared addresses (drp kNoBand = invalid -> no-op)
     auto band = [&](int drpA, int drpB) {
       const int drp = (lane < 16) ? drpA : drpB;
-      const uint32_t f = (uint32_t)(drp - 1 + boff);
-      if (blive && drp != 0 && f < (uint32_t)DP) {
+      const uint32_t f = (uint32_t)(drp + boffc);
+      if (f < (uint32_t)DP) {
         float* q = shp<float>(bbuf_s + 4u * (uint32_t)drp);
         *q -= bwt;
       }
@@ -438,29 +450,29 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
       for (int r = 0; r < NR; ++r) {
         const float4 v = make_float4(rr[4 * r], rr[4 * r + 1], rr[4 * r + 2], rr[4 * r + 3]);
         *shp<float4>(ring_s + 16u * lane + 512u * r) = v;
-        *shp<float4>(ring_s + DP * 4u + 16u * lane + 512u * r) = v;
+        *shp<float4>(ring_s + ring_b1<DP, SPARSE>() + 16u * lane + 512u * r) = v;
       }
       __syncwarp();
       band(drm, drm);
       __syncwarp();
-      band(0, r0.drp);
+      band(kNoBand, r0.drp);
     } else {
       ring_step(rr, j0 - 1, 1);
       ring_step(rr, j0, 2);
     }
     int f0 = fmean(r0), f1 = fmean(r1);
-    const int jl = j0 + nsteps - 1;
     __syncwarp();
 #pragma unroll 1
     for (int jj = 0; jj < nsteps; jj += 4) {
 #pragma unroll
       for (int half = 0; half < 2; ++half) {
         const int jA = j0 + jj + 2 * half;          // odd
-        // next pair (rows jA+2, jA+3), clamped to the run's last row jl <= k so the
-        // object-mean lookup stays in range (the pair after the last is unused)
-        const RowU n0 = rowj(min(jA + 2, jl)), n1 = rowj(min(jA + 3, jl));
+        // next pair (rows jA+2, jA+3).  After the run's last row jl <= k these are
+        // at most rows k+2, k+3 (<= h+2): their mean lookup reads M2 at n4 >= -8
+        // (inside the pad before M2) and is never used.
+        const RowU n0 = rowj(jA + 2), n1 = rowj(jA + 3);
         const int g0 = fmean(n0), g1 = fmean(n1);
-        const uint32_t ra = SPARSE ? ring_s + DP * 4u : ring_s + ((1 + 2 * half) & 3) * DP * 4u;
+        const uint32_t ra = SPARSE ? ring_s + ring_b1<DP, SPARSE>() : ring_s + ((1 + 2 * half) & 3) * DP * 4u;
         const uint32_t rb = SPARSE ? ring_s : ring_s + ((2 + 2 * half) & 3) * DP * 4u;
         const float p0 = *shp<const float>(pp_s + 4u * f0), p1 = *shp<const float>(pp_s + 4u * f1);
         const float w0 = *shp<const float>(ra + 4u * f0), w1 = *shp<const float>(rb + 4u * f1);
@@ -505,7 +517,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
     }
   };
 
-  float fr[NSW];                       // rectangle warps: W[f][32 bt] of their f slices
+  float fr[NS];                        // builder warp: W[f][32 bt] for f = lane + 32c
 
   for (int item = slot_global; item < a.items; item += gridDim.x * a.cols_per_cta) {
     const uint16_t* col = a.cols + (int64_t)item * h;
@@ -531,11 +543,11 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
         tD[v] = valid ? (uint32_t)dR + (1u << (kRBits - 1)) : 0u;
       }
       if (v <= h)                        // static record word of row v: pixel code (ordthr later)
-        cs.rec[2 * v + 1].w = (uint32_t)(dr + 1) << 16;
+        cs.rec[2 * v + 1].w = (uint32_t)(valid ? dr + 1 : kNoBand) << 16;
       if (v < 2) {                       // padding rows h+1, h+2 and row 0: T = N4 = 0
-        cs.rec[2 * (h + 1 + v) + 1] = make_uint4(0, 0, 0, 0);
+        cs.rec[2 * (h + 1 + v) + 1] = make_uint4(0, 0, 0, (uint32_t)kNoBand << 16);
         cs.rec[2 * (h + 1 + v)] = make_uint4(0, 0, 0, 0);
-        if (v == 0) { cs.rec[1].y = 0; cs.rec[1].z = 0; }
+        if (v == 0) { cs.rec[1].y = 0; cs.rec[1].z = 0; cs.tn[0] = make_uint2(0, 0); }
       }
       // E offsets of this row
       int dmr = valid ? a.D - dr : a.dmr_inv;
@@ -564,8 +576,8 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
           const uint32_t x = (w == 2) ? t : (t ? 4u : 0u);
           const uint32_t in = warp_incl_scan(x, lane) + cu;
           if (v < h) {
-            if (w == 2) cs.rec[2 * (v + 1) + 1].y = in;   // T[v+1]
-            else cs.rec[2 * (v + 1) + 1].z = in;          // N4[v+1]
+            if (w == 2) { cs.rec[2 * (v + 1) + 1].y = in; cs.tn[v + 1].x = in; }   // T[v+1]
+            else { cs.rec[2 * (v + 1) + 1].z = in; cs.tn[v + 1].y = in; }         // N4[v+1]
           }
           cu = __shfl_sync(0xffffffffu, in, 31);
         }
@@ -578,43 +590,41 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
     // anchor row 32(bt+1): a sequential prefix over rows, per f.  The
     // row offsets come from lane registers by shuffle; loads of 8 rows are issued
     // before their prefix chain.
+    // One warp (w == 1) builds them: lane l owns f = l + 32c (c < NS), so both the
+    // E' loads and the priv stores are bank-conflict free; loads of 8 rows are
+    // issued before their prefix chain.  (The other rectangle warps wait: a
+    // sequential prefix does not split well, and waiting costs no issue slots.)
     auto build_priv = [&](int bt) {
       const int K0b = bt << 5;
       const int rows = min(32, h - K0b);
       const uint32_t eor = cs.eo[K0b + min(lane, rows - 1)] >> 16;
-      const uint32_t dst_s = (uint32_t)__cvta_generic_to_shared(cs.priv) + (32 * rw + lane) * 4;
-      const uint32_t src_s = (uint32_t)__cvta_generic_to_shared(E) + (32 * rw + lane) * 4;
-      auto run = [&](auto nqc) {
-        constexpr int nq = decltype(nqc)::value;     // slices of this warp
+      const uint32_t dst_s = (uint32_t)__cvta_generic_to_shared(cs.priv) + lane * 4;
+      const uint32_t src_s = (uint32_t)__cvta_generic_to_shared(E) + lane * 4;
 #pragma unroll
-        for (int i0 = 0; i0 < 32; i0 += 8) {
-          if (i0 < rows) {
-            float x[8][nq];
+      for (int i0 = 0; i0 < 32; i0 += 8) {
+        if (i0 < rows) {
+          float x[8][NS];
 #pragma unroll
-            for (int r = 0; r < 8; ++r) {
-              const uint32_t e = __shfl_sync(0xffffffffu, eor, i0 + r);
+          for (int r = 0; r < 8; ++r) {
+            const uint32_t e = __shfl_sync(0xffffffffu, eor, i0 + r);
 #pragma unroll
-              for (int q = 0; q < nq; ++q) x[r][q] = *shp<const float>(src_s + e + 384u * q);
-            }
+            for (int c = 0; c < NS; ++c) x[r][c] = *shp<const float>(src_s + e + 128u * c);
+          }
 #pragma unroll
-            for (int r = 0; r < 8; ++r) {
-              if (i0 + r < rows) {
+          for (int r = 0; r < 8; ++r) {
+            if (i0 + r < rows) {
 #pragma unroll
-                for (int q = 0; q < nq; ++q) {
-                  fr[q] += x[r][q];
-                  *shp<float>(dst_s + ((i0 + r) * (DP + 1) + 96 * q) * 4u) = fr[q];
-                }
+              for (int c = 0; c < NS; c += 2) {
+                fadd2_inplace(fr[c], fr[c + 1], x[r][c], x[r][c + 1]);
+                *shp<float>(dst_s + ((i0 + r) * (DP + 1) + 32 * c) * 4u) = fr[c];
+                *shp<float>(dst_s + ((i0 + r) * (DP + 1) + 32 * c + 32) * 4u) = fr[c + 1];
               }
             }
           }
         }
+      }
 #pragma unroll
-        for (int q = 0; q < nq; ++q) ANg[(bt + 1) * DP + 32 * rw + 96 * q + lane] = fr[q];
-      };
-      const int nq = (NS - rw + 2) / 3;
-      if (nq == 1) run(std::integral_constant<int, 1>());
-      else if (nq == 2) run(std::integral_constant<int, (NSW >= 2 ? 2 : 1)>());
-      else run(std::integral_constant<int, NSW>());
+      for (int c = 0; c < NS; ++c) ANg[(bt + 1) * DP + 32 * c + lane] = fr[c];
     };
     // triangle cells of block bt: bottom K0+1+j', target K0+k' (k' > j'); their
     // bottoms' W-rows are the block's own priv rows: data term (absolute),
@@ -629,9 +639,9 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
         const int jp = jk & 0xff, kp = jk >> 8;
         const int k = K0b + kp;
         if (k < h) {
-          const uint4 ry = cs.rec[2 * (K0b + jp + 1) + 1];
-          const uint4 rk = cs.rec[2 * (k + 1) + 1];
-          int f = span_f(rk.y - ry.y, rk.z - ry.z, smem, Dm1);
+          const uint2 ry = cs.tn[K0b + jp + 1];
+          const uint2 rk = cs.tn[k + 1];
+          int f = span_f(rk.x - ry.x, rk.y - ry.y, smem, Dm1);
           float data = (cs.priv[kp * (DP + 1) + f] - cs.priv[jp * (DP + 1) + f]) + capQ * (float)(kp - jp);
           const uint32_t th = __ldg(a.thrg + K0b + jp + 1);
           int lvl = (f >= (int)(th & 0xffffu)) ? 1 : ((f < (int)(th >> 16)) ? 2 : 0);
@@ -646,9 +656,9 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
       }
     };
 
-    if (w != 0) {
+    if (w == 1) {
 #pragma unroll
-      for (int q = 0; q < NSW; ++q) fr[q] = 0.f;
+      for (int c = 0; c < NS; ++c) fr[c] = 0.f;
       build_priv(0);
     }
     named_bar(bar_col, kCW * 32);
@@ -656,8 +666,8 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
     // block 0 has only the j = 0 candidate (Eq. 5) and its triangle
     {
       const int kk = lane < h ? lane : h - 1;
-      const uint4 rky = cs.rec[2 * (kk + 1) + 1];
-      const uint32_t Tk = rky.y, N4k = rky.z;
+      const uint2 rky = cs.tn[kk + 1];
+      const uint32_t Tk = rky.x, N4k = rky.y;
       const float* pp = cs.priv + lane * (DP + 1);
       float rbest = INF;
       int rargj = 0x7fffffff;
@@ -687,9 +697,9 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
       if (w == 0) {
         // ============ serial warp: block b's triangle and finalisation ============
         const int kk = k < h ? k : h - 1;
-        const uint4 rky = cs.rec[2 * (kk + 1) + 1];
-        const uint32_t N4k = rky.z;
-        const uint32_t Tk = rky.y;
+        const uint2 rky = cs.tn[kk + 1];
+        const uint32_t N4k = rky.y;
+        const uint32_t Tk = rky.x;
         const float pg0 = PGg[kk], pg1 = PGg[kk + 1], ps0 = PSg[kk], ps1 = PSg[kk + 1];
         float best = INF;
         int argj = 0x7fffffff;
@@ -819,7 +829,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
                                            __float_as_uint((CGk + a.kGO_mid) - sh), __float_as_uint((CGk + a.kGO_hi) - sh));
           uint32_t* ry = reinterpret_cast<uint32_t*>(cs.rec + 2 * (k + 1) + 1);
           ry[0] = __float_as_uint((CGk + a.kGO_lo) - sh);
-          ry[3] = (rky.w & 0xffff0000u) | (uint32_t)(argf + a.ord_margin);
+          reinterpret_cast<uint16_t*>(ry + 3)[0] = (uint16_t)(argf + a.ord_margin);   // ordthr (drp kept)
           cs.argO[k] = (uint16_t)(argj | (argc << 12));
           cs.argG[k] = (uint16_t)aG;
           cs.argS[k] = (uint16_t)aS;
@@ -827,7 +837,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
         }
         if (has_next) named_bar(bar_x, kCW * 32);   // block b+1's priv rows are ready
       } else if (has_next) {
-        build_priv(bn);                  // block b's priv rows are no longer needed
+        if (w == 1) build_priv(bn);      // block b's priv rows are no longer needed
         named_bar(bar_rect, 3 * 32);
         asm volatile("bar.arrive %0, %1;" ::"r"(bar_x), "r"(kCW * 32) : "memory");
       }
@@ -839,8 +849,8 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
       const uint32_t ppn_s = (uint32_t)__cvta_generic_to_shared(ppn);
       if (has_next) {
         const int kk = Kn + lane < h ? Kn + lane : h - 1;
-        const uint4 rky = cs.rec[2 * (kk + 1) + 1];
-        Tn = rky.y; N4n = rky.z;
+        const uint2 rky = cs.tn[kk + 1];
+        Tn = rky.x; N4n = rky.y;
         if (w == 1) {                  // j = 0: first stixel spans 0..k (Eq. 5)
           int f = span_f(Tn, N4n, smem, Dm1);
           rbest = ppn[f] + a.piFirstO;
