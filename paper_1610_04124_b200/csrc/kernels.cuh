@@ -168,13 +168,20 @@ __host__ __device__ constexpr int tri_off(int jp) { return 31 * jp - (jp * (jp -
 
 __host__ __device__ inline int al16(int x) { return (x + 15) & ~15; }
 
-// Floats of W-row ring per warp.  Sparse mode: buffer 0 at 0, buffer 1 at DP + 16,
-// so the two half-warps of a band round (one per buffer, nearly equal f) fall in
-// disjoint banks.
+// Floats of W-row ring per warp.  Sparse mode: two W-row buffers, each with guard
+// entries f in [-8, 0) and [DP, DP + 24) so band rounds need no range test (f of
+// a valid pixel lies in [-8, DP + 8), the invalid code no_band() lands in
+// [DP + 8, DP + 24)); buffer 0's f = 0 at float 8, buffer 1's at DP + 56 (16 banks
+// apart, so the two half-warps of a band round -- nearly equal f -- do not
+// conflict).
 template <int DP, bool SPARSE>
-__host__ __device__ constexpr int ring_stride() { return SPARSE ? 2 * DP + 16 : 4 * DP; }
+__host__ __device__ constexpr int ring_stride() { return SPARSE ? 2 * DP + 80 : 4 * DP; }
 template <int DP, bool SPARSE>
-__host__ __device__ constexpr uint32_t ring_b1() { return (DP + 16) * 4u; }
+__host__ __device__ constexpr uint32_t ring_b0() { return SPARSE ? 8 * 4u : 0u; }
+template <int DP, bool SPARSE>
+__host__ __device__ constexpr uint32_t ring_b1() { return (DP + 48) * 4u; }   // from buffer 0
+template <int DP>
+__host__ __device__ constexpr int no_band() { return DP + 16; }   // drp code: invalid pixel
 
 template <int DP, bool SPARSE>
 __host__ __device__ inline int col_smem_bytes(int h) {
@@ -256,7 +263,6 @@ __device__ __forceinline__ void named_bar(int id, int threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
 
-constexpr int kNoBand = 0x4000;     // drp code of an invalid pixel (band update no-op)
 constexpr int kM2Pad = 16;          // bytes of shared memory before the M2 table
 
 // Object model value f of span [j, k] from prefix differences:
@@ -285,7 +291,7 @@ __device__ __forceinline__ float ldsf(uint32_t addr) {
 struct RowU {
   float AO0, AO1, AGm, AGh, AGl;   // predecessor terms of row j, shifted by -cap*j
   uint32_t T, N4;
-  int ordthr, drp;                 // drp = round(d_j) + 1, kNoBand if pixel j is invalid
+  int ordthr, drp;                 // drp = round(d_j) + 1, no_band<DP>() if pixel j is invalid
 };
 __device__ __forceinline__ RowU unpack_row(uint4 x, uint4 y) {
   RowU u;
@@ -383,10 +389,10 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
   // sparse update lanes: lanes 0-14 serve W-row buffer 1 (odd bottoms), lanes
   // 16-30 buffer 0 (even bottoms); each owns one offset d = (lane & 15) - 7 of
   // the band and its weight cap - Pair(d)
+  constexpr int kNoBand = no_band<DP>();
   const int boff = (lane & 15) - 7;
-  const float bwt = a.wt[lane & 15];
+  const float bwt = (lane & 15) < 15 ? a.wt[lane & 15] : 0.f;   // 0: write-back no-op
   // dead lanes (lane 15/31, zero weight) get an offset that puts every f out of range
-  const int boffc = ((lane & 15) < 15 && bwt != 0.f) ? boff - 1 : -0x1000;
   // ---- helpers --------------------------------------------------------------
   // dense W-row step: rr += E'[.][d_src] for f = 4*lane.. (+128 r); store to slot
   auto ring_step = [&](float (&rr)[4 * NR], int row_src, int slot) {
@@ -414,18 +420,16 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
   // explicit 32-bit offsets.
   const uint32_t rec_s = (uint32_t)__cvta_generic_to_shared(cs.rec);
   const uint32_t m2_s = (uint32_t)__cvta_generic_to_shared(M2s);   // (dynamic smem does not start at 0)
-  const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ringw);
+  const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ringw) + ring_b0<DP, SPARSE>();
   const uint32_t bbuf_s = ring_s + ((lane < 16) ? ring_b1<DP, SPARSE>() : 0u) + (uint32_t)((boff - 1) * 4);
   auto rect_run = [&](float (&rr)[4 * NR], int j0, int nsteps, uint32_t pp_s, uint32_t Tk,
                       uint32_t N4k, float& best, int& argj) {
-    // sparse band round on the shared addresses (drp kNoBand = invalid -> no-op)
+    // sparse band round: f = drp - 1 + boff always lands in the buffer or its
+    // guards (no range test; zero-weight lanes write back their value)
     auto band = [&](int drpA, int drpB) {
       const int drp = (lane < 16) ? drpA : drpB;
-      const uint32_t f = (uint32_t)(drp + boffc);
-      if (f < (uint32_t)DP) {
-        float* q = shp<float>(bbuf_s + 4u * (uint32_t)drp);
-        *q -= bwt;
-      }
+      float* q = shp<float>(bbuf_s + 4u * (uint32_t)drp);
+      *q -= bwt;
     };
     auto rowj = [&](int j) {
       const uint4* q = shp<const uint4>(rec_s + 32u * (uint32_t)j);
