@@ -364,7 +364,8 @@ int stixels_create(const stixels_params* params, int width, int height, int max_
   };
   int cb = DPv == 128 ? (sparse ? col_smem_bytes<128, true>(height) : col_smem_bytes<128, false>(height))
                       : (sparse ? col_smem_bytes<256, true>(height) : col_smem_bytes<256, false>(height));
-  int sb = stx::kM2Pad + al16((height + 1) * 4) + 4 * esz * 4 + al16(kTri * 2);   // pad, M2, E copies, triangle decode
+  int sb = stx::kM2Pad + al16((height + 1) * 4) + (sparse ? stx::e_copies<true>() : stx::e_copies<false>()) * esz * 4 +
+           al16(kTri * 2);   // pad, M2, E copies, triangle decode
   int cpc = std::min(4, (optin - sb) / cb);   // columns per CTA (4 warps each)
   if (cpc < 1) return bail(STIXELS_ERR_UNSUPPORTED, "per-column shared memory exceeds the SM");
   h->cols_per_cta = cpc;

@@ -126,7 +126,7 @@ struct DPArgs {
   int32_t* count;          // [items]
   float* col_cost;         // [items] or null
   float* scratch;          // [grid*cols_per_cta][2][h+1]  ground / sky prefix sums
-  const float* E;          // [4][esz] object pair-cost windows (host built)
+  const float* E;          // [4][esz] object pair-cost windows (host built; sparse mode loads copy 0)
   const uint32_t* M2;      // [h+1] magic reciprocals ceil(2^31/n)
   const float* gG;         // ground cost by |dR - dgR|, length LG (last = cap)
   const float* gS;         // sky cost by dR, length LS (last = cap)
@@ -182,6 +182,10 @@ template <int DP, bool SPARSE>
 __host__ __device__ constexpr uint32_t ring_b1() { return (DP + 48) * 4u; }   // from buffer 0
 template <int DP>
 __host__ __device__ constexpr int no_band() { return DP + 16; }   // drp code: invalid pixel
+// E' copies in shared memory: the dense ring reads 4 shifted copies, the sparse
+// path (build only) one.
+template <bool SPARSE>
+__host__ __device__ constexpr int e_copies() { return SPARSE ? 1 : 4; }
 
 template <int DP, bool SPARSE>
 __host__ __device__ inline int col_smem_bytes(int h) {
@@ -369,9 +373,9 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
   // bytes before it (their value is never used)
   uint32_t* M2s = reinterpret_cast<uint32_t*>(smem + kM2Pad);
   float* E = reinterpret_cast<float*>(smem + kM2Pad + al16((h + 1) * 4));
-  uint16_t* tri_jk = reinterpret_cast<uint16_t*>(smem + kM2Pad + al16((h + 1) * 4) + 4 * a.esz * 4);
+  uint16_t* tri_jk = reinterpret_cast<uint16_t*>(smem + kM2Pad + al16((h + 1) * 4) + e_copies<SPARSE>() * a.esz * 4);
   for (int i = threadIdx.x; i <= h; i += blockDim.x) M2s[i] = a.M2[i];
-  for (int i = threadIdx.x; i < 4 * a.esz; i += blockDim.x) E[i] = a.E[i];
+  for (int i = threadIdx.x; i < e_copies<SPARSE>() * a.esz; i += blockDim.x) E[i] = a.E[i];
   for (int jp = 0; jp < 31; ++jp)                 // triangle cell index -> (j', k')
     for (int kp = jp + 1 + (int)threadIdx.x; kp < 32; kp += blockDim.x)
       tri_jk[tri_off(jp) + kp - jp - 1] = (uint16_t)(jp | (kp << 8));
@@ -391,7 +395,10 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
   // the band and its weight cap - Pair(d)
   constexpr int kNoBand = no_band<DP>();
   const int boff = (lane & 15) - 7;
-  const float bwt = (lane & 15) < 15 ? a.wt[lane & 15] : 0.f;   // 0: write-back no-op
+  const float bwt = a.wt[lane & 15];
+  // lanes 15/31 sit out (a loop-invariant predicate): with them each half-warp
+  // would span 16 banks and the two halves would collide whenever their f differ
+  const bool blive = (lane & 15) < 15;
   // dead lanes (lane 15/31, zero weight) get an offset that puts every f out of range
   // ---- helpers --------------------------------------------------------------
   // dense W-row step: rr += E'[.][d_src] for f = 4*lane.. (+128 r); store to slot
@@ -429,7 +436,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
     auto band = [&](int drpA, int drpB) {
       const int drp = (lane < 16) ? drpA : drpB;
       float* q = shp<float>(bbuf_s + 4u * (uint32_t)drp);
-      *q -= bwt;
+      if (blive) *q -= bwt;
     };
     auto rowj = [&](int j) {
       const uint4* q = shp<const uint4>(rec_s + 32u * (uint32_t)j);
