@@ -72,6 +72,10 @@ def lib():
         L.orc_reduce.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                  ctypes.c_longlong, ctypes.c_int, ctypes.c_int, ctypes.c_uint,
                                  ctypes.c_int, ctypes.c_int, ctypes.c_void_p]
+        L.orc_reduce_median.restype = None
+        L.orc_reduce_median.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                 ctypes.c_longlong, ctypes.c_int, ctypes.c_int, ctypes.c_uint,
+                                 ctypes.c_int, ctypes.c_int, ctypes.c_void_p]
         for name in ("orc_cost_sky",):
             getattr(L, name).restype = ctypes.c_double
             getattr(L, name).argtypes = [P(_Model), ctypes.c_int]
@@ -166,14 +170,16 @@ def ground_R(model: Model, v: int) -> int:
     return lib().orc_ground_R(ctypes.byref(model.c()), v)
 
 
-def reduce(img: np.ndarray, s: int, q_bits: int, invalid: int, D: int, R_bits: int = 8):
-    """img: [H][W] uint8/uint16 -> [n_cols][H] int32 reduced columns (model order)."""
+def reduce(img: np.ndarray, s: int, q_bits: int, invalid: int, D: int, R_bits: int = 8,
+           mode: int = 0):
+    """img: [H][W] uint8/uint16 -> [n_cols][H] int32 reduced columns (model order).
+    mode 0: mean of the valid pixels; 1: their median (NEXT f4, L#24)."""
     img = np.ascontiguousarray(img)
     H, W = img.shape
     n_cols = W // s
     out = np.zeros((n_cols, H), dtype=np.int32)
-    lib().orc_reduce(img.ctypes.data, img.itemsize, W, H, W, s, q_bits, invalid, D, R_bits,
-                     out.ctypes.data)
+    fn = lib().orc_reduce if mode == 0 else lib().orc_reduce_median
+    fn(img.ctypes.data, img.itemsize, W, H, W, s, q_bits, invalid, D, R_bits, out.ctypes.data)
     return out
 
 

@@ -148,6 +148,54 @@ void orc_reduce(const void* img, int bytes_per_px, int W, int H, long long pitch
 }
 
 /* --------------------------------------------------------------------------
+ * Median column reduction (NEXT row f4 of SURVEY 8(f); BASELINE north_star
+ * "median/mean" reduction of the s pixels; reading L#24): the median
+ * of the VALID pixels among the s of a row segment -- the middle value of the
+ * sorted valid values, the mean of the two middle values when their count is
+ * even -- in units of 1/2^R_bits, rounded half up exactly like the mean
+ * (orc_reduce with the middle value(s) as the summands).  All invalid -> -1.
+ * Written the plain way: collect, sort (qsort), pick.
+ * ------------------------------------------------------------------------ */
+static int cmp_uint(const void* a, const void* b) {
+  unsigned int x = *(const unsigned int*)a, y = *(const unsigned int*)b;
+  return (x > y) - (x < y);
+}
+
+void orc_reduce_median(const void* img, int bytes_per_px, int W, int H, long long pitch_px,
+                       int s, int Q_bits, unsigned int invalid, int D, int R_bits, int* out) {
+  int n_cols = W / s;
+  unsigned int* vals = (unsigned int*)malloc(sizeof(unsigned int) * (size_t)(s > 0 ? s : 1));
+  for (int c = 0; c < n_cols; ++c) {
+    for (int r = 0; r < H; ++r) {
+      int n = 0;
+      for (int x = c * s; x < c * s + s; ++x) {
+        unsigned int u;
+        if (bytes_per_px == 1)
+          u = ((const uint8_t*)img)[(long long)r * pitch_px + x];
+        else
+          u = ((const uint16_t*)img)[(long long)r * pitch_px + x];
+        if (u == invalid) continue;
+        if ((long long)u >= ((long long)D << Q_bits)) continue; /* d >= D: invalid */
+        vals[n++] = u;
+      }
+      int v = H - 1 - r;
+      if (n == 0) {
+        out[(long long)c * H + v] = -1;
+        continue;
+      }
+      qsort(vals, (size_t)n, sizeof(unsigned int), cmp_uint);
+      long long sum, cnt;
+      if (n % 2) { sum = vals[n / 2]; cnt = 1; }
+      else { sum = (long long)vals[n / 2 - 1] + vals[n / 2]; cnt = 2; }
+      long long num = 2 * (sum << R_bits) + (cnt << Q_bits);
+      long long den = 2 * (cnt << Q_bits);
+      out[(long long)c * H + v] = (int)(num / den);
+    }
+  }
+  free(vals);
+}
+
+/* --------------------------------------------------------------------------
  * Per-pixel data costs (Eq. 4 per class).
  *  ground: f = f_ground(v) (fixed point); sky: f = 0;
  *  object: f integer mean, measured disparity rounded half up to an
