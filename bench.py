@@ -47,6 +47,10 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-frames", type=int, default=0, help="oracle sample size (0 = auto)")
+    ap.add_argument("--sweep", action="store_true",
+                    help="NEXT f1: resolution / stixel-width sweep with fps/W (one JSON line "
+                         "per config; not the driver's bench line)")
+    ap.add_argument("--sweep-out", default="", help="also write the sweep lines to this file")
     return ap.parse_args()
 
 
@@ -127,13 +131,15 @@ class ClockSampler:
                 self.proc.wait(2)
             except Exception:
                 self.proc.kill()
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        num = lambda x: x.replace(".", "").isdigit()
+        sm = [float(r[0]) for r in self.rows if num(r[0])]
+        mx = [float(r[1]) for r in self.rows if num(r[1])]
+        pw = [float(r[2]) for r in self.rows if num(r[2])]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i] == "Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.rows)}
+                "power_w": statistics.median(pw) if pw else None, "samples": len(self.rows)}
 
 
 def measured_peaks():
@@ -210,6 +216,86 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+SWEEP = [  # (W, H, s, D): C4 stixel widths, then resolutions at s=5 (fig:fps)
+    (1024, 440, 3, 128), (1024, 440, 5, 128), (1024, 440, 7, 128), (1024, 440, 10, 128),
+    (512, 440, 5, 128), (2048, 440, 5, 128),             # width: linear
+    (1024, 220, 5, 128), (1024, 880, 5, 128),             # height: quadratic
+    (640, 480, 5, 128), (1280, 480, 5, 128),              # the paper's quoted 1280x480
+    (2048, 1024, 5, 256),                                  # C5 (per GPU)
+]
+
+
+def run_sweep(args, local):
+    """NEXT f1: fps and fps/W over resolutions and stixel widths,
+    each config with sampled exact parity against the oracle.  Power is the
+    median nvidia-smi power.draw during the timed region."""
+    import torch
+    from paper_1610_04124_b200 import stixels as S
+    from inputs import synth
+    from oracle import oracle as orc
+    from tests import modelparams as mp
+    from tests.gpuharness import compare_exact
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.Stream(dev)
+    lines = []
+    for (W, H, s, D) in SWEEP:
+        p = mp.make(max_disparity=D, stixel_width=s,
+                    ground_slope=0.35 if D == 256 else 0.4)
+        if D == 256:
+            p["cost_frac_bits"] = 10                          # L#22: q=10 for C5
+        cells = (W // s) * H * (H + 1) // 2
+        B = int(max(16, min(4096, 0.2 * 4e11 / cells)))     # ~0.2 s per batch at ~4e11 cells/s
+        nd = min(16, B)
+        pool = np.stack([synth.frame(4, i, W, H, D, alpha=p["ground_slope"]) for i in range(nd)])
+        disp = torch.from_numpy(pool.view(np.int16)).to(dev)[torch.arange(B) % nd]
+        hd = S.Handle(S.params_from_dict(p, H), W, H, B, device=local, stream=stream)
+        out, cnt, cost = hd.alloc_outputs(B)
+        with torch.cuda.stream(stream):
+            for _ in range(max(3, args.warmup)):
+                hd.compute(disp, out, cnt, cost)
+        torch.cuda.synchronize()
+        # sampled parity: 2 frames x 6 columns
+        m = mp.oracle_model(p, H)
+        rng = np.random.default_rng(W + H + s)
+        got = S.decode(out[:2].cpu().numpy(), cnt[:2].cpu().numpy())
+        ch = cost[:2].cpu().numpy()
+        bad = 0
+        for f in range(2):
+            ci = rng.choice(hd.n_cols, 6, replace=False)
+            rc = orc.reduce(pool[f], s, 4, 0xFFFF, D)[ci]
+            st, oc = orc.solve_frame(m, rc)
+            bad += len(compare_exact([[got[f][c] for c in ci]], [ch[f][ci]], [st], [oc],
+                                     p["cost_frac_bits"]))
+        steps = max(3, args.steps)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        sampler = ClockSampler(local)
+        sampler.start()
+        time.sleep(0.3)
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            for _ in range(steps):
+                hd.compute(disp, out, cnt, cost)
+            e1.record(stream)
+        torch.cuda.synchronize()
+        clocks = sampler.stop()
+        ms = e0.elapsed_time(e1) / steps
+        fps = B / (ms / 1000.0)
+        line = {"sweep": "f1", "W": W, "H": H, "s": s, "D": D, "batch": B, "fps": fps,
+                "ms_per_batch": ms, "cells_per_s": cells * fps,
+                "power_w": clocks.get("power_w"),
+                "fps_per_watt": fps / clocks["power_w"] if clocks.get("power_w") else None,
+                "clocks": clocks,
+                "parity": "exact (12 sampled columns)" if bad == 0 else f"MISMATCH {bad}/12"}
+        lines.append(line)
+        print(json.dumps(line), flush=True)
+        hd.destroy()
+        del disp
+    if args.sweep_out:
+        with open(args.sweep_out, "w") as fo:
+            for line in lines:
+                fo.write(json.dumps(line) + "\n")
+
+
 def main():
     args = parse()
     rank, world, local = dist_env()
@@ -228,6 +314,10 @@ def main():
     from paper_1610_04124_b200 import build as b
     b.build()
     from paper_1610_04124_b200 import stixels as S
+    if args.sweep:
+        if rank == 0:
+            run_sweep(args, local)
+        return
 
     p = params_dict()
     B = args.batch
@@ -370,6 +460,7 @@ def main():
             "stage_share": {"reduce": sum(red) / total_ms, "dp": sum(dp) / total_ms},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": 2 * args.steps, "clocks": clocks, "parity": parity,
+            "fps_per_watt": (value / world / clocks["power_w"]) if clocks.get("power_w") else None,
         }
         print(json.dumps(line), flush=True)
     hd.destroy()

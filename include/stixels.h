@@ -48,6 +48,12 @@ extern "C" {
 #define STIXELS_U8 0  /* uint8 fixed point, disp_frac_bits fractional bits  */
 #define STIXELS_U16 1 /* uint16 fixed point, disp_frac_bits fractional bits */
 
+/* ---- column reduction (a2) ---------------------------------------------- */
+#define STIXELS_REDUCE_MEAN 0   /* mean of the valid pixels of the s-wide segment */
+#define STIXELS_REDUCE_MEDIAN 1 /* their median; mean of the two middle values when the
+                                   count is even; same half-up rounding to 1/256 (NEXT
+                                   f4, L#24); stixel_width <= 64           */
+
 /* ---- classes ------------------------------------------------------------- */
 #define STIXELS_GROUND 0
 #define STIXELS_OBJECT 1
@@ -94,7 +100,7 @@ typedef struct stixels_params {
   int32_t disp_frac_bits;/* Q: fractional bits of the input, 0..8                 */
   uint32_t invalid_value;/* sentinel of an invalid pixel; values decoding to >= D
                             are invalid too (L#23)                                */
-  int32_t reduce_mode;   /* 0 = mean of valid pixels; others reserved     */
+  int32_t reduce_mode;   /* STIXELS_REDUCE_MEAN or STIXELS_REDUCE_MEDIAN  */
   /* --- numerics -------------------------------------------------------------- */
   int32_t cost_frac_bits;/* q: costs are integers in units of 2^-q nats ("exact
                             mode", L#22); 0 = continuous fp32 Eq. 4            */

@@ -162,7 +162,12 @@ int validate(const stixels_params* p, int W, int H, int max_batch, std::string& 
   }
   if (p->disp_format != STIXELS_U8 && p->disp_format != STIXELS_U16) { msg = "disp_format must be U8 or U16"; return STIXELS_ERR_PARAM; }
   if (p->disp_frac_bits < 0 || p->disp_frac_bits > 8) { msg = "disp_frac_bits must be in [0, 8]"; return STIXELS_ERR_PARAM; }
-  if (p->reduce_mode != 0) { msg = "only reduce_mode 0 (mean, P:195) is implemented"; return STIXELS_ERR_UNSUPPORTED; }
+  if (p->reduce_mode != STIXELS_REDUCE_MEAN && p->reduce_mode != STIXELS_REDUCE_MEDIAN) {
+    msg = "reduce_mode must be STIXELS_REDUCE_MEAN (P:195) or STIXELS_REDUCE_MEDIAN"; return STIXELS_ERR_UNSUPPORTED;
+  }
+  if (p->reduce_mode == STIXELS_REDUCE_MEDIAN && p->stixel_width > kMedianMaxS) {
+    msg = "the median reduction supports stixel_width <= 64"; return STIXELS_ERR_UNSUPPORTED;
+  }
   if (p->cost_frac_bits < 0 || p->cost_frac_bits > 20) { msg = "cost_frac_bits must be in [0, 20]"; return STIXELS_ERR_PARAM; }
   if (p->max_stixels < 0) { msg = "max_stixels must be >= 0"; return STIXELS_ERR_PARAM; }
   return STIXELS_OK;
@@ -423,6 +428,7 @@ static int launch_reduce(stixels_handle* h, const void* d_disp, int64_t pitch, i
   r.s = h->p.stixel_width; r.tc = h->red_tc; r.q_bits = h->p.disp_frac_bits; r.D = h->p.max_disparity;
   r.bpp = h->p.disp_format == STIXELS_U16 ? 2 : 1;
   r.invalid = h->p.invalid_value;
+  r.median = h->p.reduce_mode == STIXELS_REDUCE_MEDIAN;
   r.out = d_cols;
   dim3 grid((h->n_cols + h->red_tc - 1) / h->red_tc, (h->H + kRedRows - 1) / kRedRows, batch);
   reduce_kernel<<<grid, kRedThreads, h->red_smem, s>>>(r);

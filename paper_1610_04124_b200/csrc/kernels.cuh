@@ -42,8 +42,10 @@ struct ReduceArgs {
   int64_t pitch;        // bytes
   int W, H, n_cols, s, tc, q_bits, D, bpp;
   uint32_t invalid;
+  int median;           // 0: mean of the valid pixels; 1: their median (f4)
   uint16_t* out;        // [batch][n_cols][H], 0xFFFF = invalid
 };
+constexpr int kMedianMaxS = 64;
 
 __global__ void __launch_bounds__(kRedThreads) reduce_kernel(ReduceArgs a) {
   extern __shared__ uint16_t tile[];             // [kRedRows][tpx + 1]
@@ -80,6 +82,27 @@ __global__ void __launch_bounds__(kRedThreads) reduce_kernel(ReduceArgs a) {
       bool ok = (u != a.invalid) && (u < lim);
       sum += ok ? u : 0u;
       n += ok ? 1u : 0u;
+    }
+    if (a.median && n) {
+      // median of the n valid values (L#24): the values of ranks (n-1)/2 and n/2
+      // by rank counting (s <= 64, no sort), averaged with the mean's rounding
+      const uint32_t k1 = (n - 1) >> 1, k2 = n >> 1;
+      uint32_t va = 0, vb = 0;
+      for (int x = 0; x < a.s; ++x) {
+        const uint32_t u = p[x];
+        if (u == a.invalid || u >= lim) continue;
+        uint32_t less = 0, leq = 0;
+        for (int y = 0; y < a.s; ++y) {
+          const uint32_t t = p[y];
+          const bool ok = (t != a.invalid) && (t < lim);
+          less += (ok && t < u) ? 1u : 0u;
+          leq += (ok && t <= u) ? 1u : 0u;
+        }
+        if (less <= k1 && k1 < leq) va = u;
+        if (less <= k2 && k2 < leq) vb = u;
+      }
+      sum = va + vb;
+      n = 2;
     }
     uint16_t val = 0xFFFF;
     if (n) {

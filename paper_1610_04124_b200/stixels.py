@@ -16,6 +16,7 @@ from .build import LIB
 
 GROUND, OBJECT, SKY = 0, 1, 2
 U8, U16 = 0, 1
+REDUCE_MEAN, REDUCE_MEDIAN = 0, 1
 
 OK, ERR_ARG, ERR_PARAM, ERR_UNSUPPORTED, ERR_CUDA, ERR_CAPACITY = 0, -1, -2, -3, -4, -5
 
@@ -110,6 +111,7 @@ def params_from_dict(d: dict, H: int) -> Params:
     p.invalid_value = int(d["invalid_value"])
     p.cost_frac_bits = int(d["cost_frac_bits"])
     p.max_stixels = int(d.get("max_stixels", 0))
+    p.reduce_mode = int(d.get("reduce_mode", REDUCE_MEAN))
     return p
 
 

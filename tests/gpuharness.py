@@ -40,7 +40,7 @@ def run_oracle(p: dict, frames: np.ndarray, cols_subset=None, threads: int = 0):
     res, costs = [], []
     for b in range(B):
         cols = orc.reduce(frames[b], p["stixel_width"], p["disp_frac_bits"],
-                          p["invalid_value"], p["max_disparity"])
+                          p["invalid_value"], p["max_disparity"], mode=p.get("reduce_mode", 0))
         if cols_subset is not None:
             cols = cols[cols_subset[b]]
         st, c = orc.solve_frame(m, cols, mode=1, threads=threads)

@@ -45,6 +45,35 @@ def test_reduce_bit_exact():
         assert (got[b] == want).all()
 
 
+@pytest.mark.parametrize("s", [1, 2, 5, 8, 13])
+def test_reduce_median_bit_exact(s):
+    """Median reduction (NEXT f4): every reduced value equals the oracle's
+    (sort-based) median, odd and even valid counts, invalid and >= D pixels."""
+    import torch
+    from oracle import oracle as orc
+    from paper_1610_04124_b200 import stixels as S
+    rng = np.random.default_rng(40 + s)
+    H, W, D = 75, 13 * s + 3, 64
+    f = rng.integers(0, (D + 3) * 16, size=(2, H, W)).astype(np.uint16)
+    f[rng.random(f.shape) < 0.15] = 0xFFFF
+    p = mp.make(max_disparity=D, stixel_width=s, reduce_mode=1)
+    hd = S.Handle(S.params_from_dict(p, H), W, H, 2)
+    cols = torch.empty((2, hd.n_cols, H), dtype=torch.int16, device="cuda")
+    hd.reduce(torch.from_numpy(f.view(np.int16)).cuda(), cols)
+    hd.sync()
+    got = cols.cpu().numpy().view(np.uint16).astype(np.int32)
+    got[got == 0xFFFF] = -1
+    for b in range(2):
+        assert (got[b] == orc.reduce(f[b], s, 4, 0xFFFF, D, mode=1)).all()
+
+
+def test_median_mode_end_to_end_exact():
+    """Whole path with the median reduction: identical lists and costs."""
+    frames = _frames_c2(2, seed0=2500)
+    p = mp.make(reduce_mode=1)
+    _assert_exact(p, frames)
+
+
 def test_c1_scene_exact():
     sc = synth.c1_scene()
     frames = np.stack([synth.render(sc, 1, noise=False), synth.render(sc, 2)])
@@ -68,6 +97,16 @@ def test_shapes_and_disparity_ranges_exact(H, W, D, s):
                       [synth.render(synth.random_scene(90, W, H, D, alpha=0.9 * D / max(H, 2)),
                                     90)])
     p = mp.make(max_disparity=D, stixel_width=s, ground_slope=0.9 * D / max(H, 2))
+    _assert_exact(p, frames)
+
+
+def test_max_height_c5_shape_exact():
+    """Maximum column height h = 1024 with D = 256 (config C5's shape, q = 10 per
+    L#22): 2 frames of 9 columns, every column exact."""
+    H, W, D = 1024, 47, 256
+    p = mp.make(max_disparity=D, ground_slope=0.35, cost_frac_bits=10)
+    frames = np.stack([synth.render(synth.random_scene(700 + i, W, H, D, alpha=0.35), 700 + i)
+                       for i in range(2)])
     _assert_exact(p, frames)
 
 

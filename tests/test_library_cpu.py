@@ -62,7 +62,7 @@ def _create(p, W=1024, H=440, B_=1):
     ("p_out", 0.0, S.ERR_PARAM), ("p_out", 1.0, S.ERR_PARAM), ("max_disparity", 1, S.ERR_PARAM),
     ("max_disparity", 300, S.ERR_UNSUPPORTED), ("stixel_width", 0, S.ERR_PARAM),
     ("a_norm", 0.0, S.ERR_PARAM), ("p_ord", 1.5, S.ERR_PARAM), ("ord_margin", -1, S.ERR_PARAM),
-    ("disp_frac_bits", 9, S.ERR_PARAM), ("reduce_mode", 1, S.ERR_UNSUPPORTED),
+    ("disp_frac_bits", 9, S.ERR_PARAM), ("reduce_mode", 2, S.ERR_UNSUPPORTED),
     ("cost_frac_bits", 30, S.ERR_PARAM), ("horizon_row", float("inf"), S.ERR_PARAM),
 ])
 def test_param_validation(field, value, code):
@@ -83,6 +83,13 @@ def test_structural_zeros_enforced():
     assert _create(p, W=4) == S.ERR_ARG     # width < s
     assert _create(p, H=2000) == S.ERR_UNSUPPORTED
     assert _create(p, B_=0) == S.ERR_ARG
+
+
+def test_median_width_limit():
+    p = S.default_params()
+    p.reduce_mode = S.REDUCE_MEDIAN
+    p.stixel_width = 65
+    assert _create(p, W=1040) == S.ERR_UNSUPPORTED
 
 
 def test_exact_mode_range_guard():
