@@ -101,6 +101,25 @@ def clean_disparity(sc: Scene) -> np.ndarray:
     return d
 
 
+def gt_labels(sc: Scene) -> np.ndarray:
+    """Ground-truth label map [H][W] of the scene (for the NEXT f3 quality
+    metrics): -1 = ground, -2 = sky, k >= 0 = the box k visible at that pixel
+    (the same nearest-wins painting as clean_disparity)."""
+    r = np.arange(sc.H, dtype=np.float64)[:, None]
+    d = np.broadcast_to(ground_disparity_image_row(sc.alpha, sc.horizon_row, r),
+                        (sc.H, sc.W)).copy()
+    sky = np.broadcast_to(np.arange(sc.H)[:, None] <= sc.horizon_row, (sc.H, sc.W))
+    d[sky] = np.nan
+    lab = np.where(sky, -2, -1).astype(np.int32)
+    for k, b in enumerate(sc.boxes):
+        r0 = max(0, b.base_row - b.height + 1)
+        blk = d[r0:b.base_row + 1, b.x0:b.x1]
+        nearer = np.isnan(blk) | (blk <= b.disp)
+        blk[nearer] = b.disp
+        lab[r0:b.base_row + 1, b.x0:b.x1][nearer] = k
+    return lab
+
+
 def render(sc: Scene, seed: int, noise: bool = True) -> np.ndarray:
     """u16 fixed-point disparity image [H][W] with `q_bits` fractional bits."""
     rng = np.random.Generator(np.random.PCG64(seed ^ 0x5EED))
