@@ -45,6 +45,7 @@ class _Model(ctypes.Structure):
         ("p_exist", ctypes.c_double),
         ("ord_margin", ctypes.c_int), ("grav_margin", ctypes.c_int),
         ("alpha", ctypes.c_double), ("horizon_row", ctypes.c_double),
+        ("sigma_o_f", ctypes.c_void_p), ("sigma_g_v", ctypes.c_void_p),
     ]
 
 
@@ -141,6 +142,8 @@ class Model:
     grav_margin: int = 1
     alpha: float = 0.4
     horizon_row: float = 0.0
+    sigma_o_f: np.ndarray | None = None   # NEXT f2: sigma_O(f), D entries (None: constant)
+    sigma_g_v: np.ndarray | None = None   # NEXT f2: sigma_G(v), h entries (None: constant)
 
     def c(self) -> _Model:
         m = _Model()
@@ -154,6 +157,13 @@ class Model:
         m.p_ord, m.p_grav, m.p_blg, m.p_exist = self.p_ord, self.p_grav, self.p_blg, self.p_exist
         m.ord_margin, m.grav_margin = self.ord_margin, self.grav_margin
         m.alpha, m.horizon_row = self.alpha, self.horizon_row
+        # the double arrays must outlive the struct: keep them on the model
+        self._so = None if self.sigma_o_f is None else np.ascontiguousarray(self.sigma_o_f, np.float64)
+        self._sg = None if self.sigma_g_v is None else np.ascontiguousarray(self.sigma_g_v, np.float64)
+        assert self._so is None or len(self._so) == self.D
+        assert self._sg is None or len(self._sg) == self.h
+        m.sigma_o_f = None if self._so is None else self._so.ctypes.data
+        m.sigma_g_v = None if self._sg is None else self._sg.ctypes.data
         return m
 
 

@@ -48,6 +48,11 @@ typedef struct {
   int ord_margin, grav_margin;          /* disparity margins (L#1) */
   double alpha;       /* ground slope (disparity per row) */
   double horizon_row; /* image row of the horizon (0 = top) */
+  /* NEXT f2: the noise model sigma^c(f, v) of Eq. 4 as tables, NULL =
+   * the per-class constant above (L#2): sigma_O of the object's disparity f
+   * (D entries) and sigma_G of the model row v (h entries). */
+  const double* sigma_o_f;
+  const double* sigma_g_v;
 } orc_model;
 
 typedef struct {
@@ -209,7 +214,7 @@ double orc_cost_ground(const orc_model* m, int dR, int v) {
   if (dR < 0) return qz(m, cap_cost(m));
   double R = (double)(1 << m->R_bits);
   double delta = (double)((long long)dR - orc_ground_R(m, v)) / R;
-  return qz(m, orc_eq4(m, delta, m->sigma[ORC_G]));
+  return qz(m, orc_eq4(m, delta, m->sigma_g_v ? m->sigma_g_v[v] : m->sigma[ORC_G]));
 }
 double orc_cost_sky(const orc_model* m, int dR) {
   if (dR < 0) return qz(m, cap_cost(m));
@@ -223,7 +228,7 @@ int orc_round_disp(const orc_model* m, int dR) {
 double orc_cost_object(const orc_model* m, int dR, int f) {
   if (dR < 0) return qz(m, cap_cost(m));
   double delta = (double)(orc_round_disp(m, dR) - f);
-  return qz(m, orc_eq4(m, delta, m->sigma[ORC_O]));
+  return qz(m, orc_eq4(m, delta, m->sigma_o_f ? m->sigma_o_f[f] : m->sigma[ORC_O]));
 }
 
 /* --------------------------------------------------------------------------
