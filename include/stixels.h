@@ -105,6 +105,13 @@ typedef struct stixels_params {
   int32_t cost_frac_bits;/* q: costs are integers in units of 2^-q nats ("exact
                             mode", L#22); 0 = continuous fp32 Eq. 4            */
   int32_t max_stixels;   /* per-column output capacity; 0 = h (never overflows)   */
+  /* --- NEXT f2: the noise model sigma^c(f, v) of P:108 as tables (host memory,
+         read by stixels_create only; NULL = the per-class constant sigma[]) --- */
+  const float* sigma_object_f; /* D entries: sigma_O of the object disparity f;
+                                  Pair[f][d] becomes a genuine D x D table.
+                                  Its band (|d - f| with Pair < cap) must be <= 7
+                                  disparities, else UNSUPPORTED                   */
+  const float* sigma_ground_v; /* height entries: sigma_G of model row v           */
 } stixels_params;
 
 /* One output stixel (L#19): rows [bottom, top] (bottom <= top, model

@@ -26,9 +26,12 @@ struct stixels_handle {
   cudaStream_t stream = nullptr;
   int n_cols = 0, cap = 0, dp_slots = 128, cols_per_cta = 0, smem = 0, grid = 0, sms = 0;
   bool sparse = true;
+  bool pair2d = false;          // NEXT f2: sigma_O(f) table given
   int red_tc = 0, red_smem = 0;
   DPArgs args{};
   float* d_E = nullptr;
+  float* d_E2 = nullptr;        // NEXT f2: [D+2][DP] 2-D pair table
+  float* d_WT = nullptr;        // NEXT f2: [DP+17][16] band weights
   uint32_t* d_M2 = nullptr;
   float* d_gG = nullptr;
   float* d_gS = nullptr;
@@ -213,7 +216,7 @@ const char* stixels_last_error(const stixels_handle* h) {
 }
 
 static void free_all(stixels_handle* h) {
-  cudaFree(h->d_E); cudaFree(h->d_M2); cudaFree(h->d_gG); cudaFree(h->d_gS);
+  cudaFree(h->d_E); cudaFree(h->d_E2); cudaFree(h->d_WT); cudaFree(h->d_M2); cudaFree(h->d_gG); cudaFree(h->d_gS);
   cudaFree(h->d_dgR); cudaFree(h->d_thr); cudaFree(h->d_overflow); cudaFree(h->d_cols); cudaFree(h->d_scratch);
   for (int i = 0; i < 2; ++i) {
     cudaFree(h->hin[i]); cudaFree(h->hout[i]); cudaFree(h->hcnt[i]); cudaFree(h->hcost[i]);
@@ -252,19 +255,51 @@ int stixels_create(const stixels_params* params, int width, int height, int max_
   const double capQ = hm.Q(hm.cap());
   const int R = 256;
   std::vector<float> gG, gS;
-  // ground / sky cost by distance to the model disparity in 1/256 units
-  for (int i = 0;; ++i) {
-    double v = hm.Q(hm.eq4((double)i / R, (double)params->sigma[0]));
-    gG.push_back((float)v);
-    if (v >= capQ || i > D * R) break;
+  // NEXT f2 noise-model tables (host copies; the caller's arrays are read here only)
+  std::vector<double> sig_o, sig_g;
+  if (params->sigma_object_f) {
+    for (int f = 0; f < D; ++f) {
+      const float x = params->sigma_object_f[f];
+      if (!(x > 0.f) || !std::isfinite(x)) return bail(STIXELS_ERR_PARAM, "sigma_object_f entries must be finite and > 0");
+      sig_o.push_back((double)x);
+    }
+  }
+  if (params->sigma_ground_v) {
+    for (int v = 0; v < height; ++v) {
+      const float x = params->sigma_ground_v[v];
+      if (!(x > 0.f) || !std::isfinite(x)) return bail(STIXELS_ERR_PARAM, "sigma_ground_v entries must be finite and > 0");
+      sig_g.push_back((double)x);
+    }
+  }
+  h->p.sigma_object_f = nullptr;   // the handle keeps no caller pointers
+  h->p.sigma_ground_v = nullptr;
+  // ground / sky cost by distance to the model disparity in 1/256 units; with a
+  // per-row sigma_G(v) one table per row, all of the longest row's length
+  int LGr = 0;
+  {
+    const int nrows = sig_g.empty() ? 1 : height;
+    std::vector<std::vector<float>> rows(nrows);
+    for (int r = 0; r < nrows; ++r) {
+      const double sg = sig_g.empty() ? (double)params->sigma[0] : sig_g[r];
+      for (int i = 0;; ++i) {
+        double v = hm.Q(hm.eq4((double)i / R, sg));
+        rows[r].push_back((float)v);
+        if (v >= capQ || i > D * R) break;
+      }
+      rows[r].back() = (float)capQ;
+      LGr = std::max(LGr, (int)rows[r].size());
+    }
+    for (int r = 0; r < nrows; ++r) {
+      rows[r].resize(LGr, (float)capQ);   // beyond a row's own table: the cap
+      gG.insert(gG.end(), rows[r].begin(), rows[r].end());
+    }
   }
   for (int i = 0;; ++i) {
     double v = hm.Q(hm.eq4((double)i / R, (double)params->sigma[2]));
     gS.push_back((float)v);
     if (v >= capQ || i > D * R) break;
   }
-  gG.back() = (float)capQ;   // clamp index -> cap (monotone Eq. 4)
-  gS.back() = (float)capQ;
+  gS.back() = (float)capQ;   // clamp index -> cap (monotone Eq. 4)
   // object pair-cost LUT Pair[f][d] = Eq4(d - f, sigma_O), stored shifted by
   // the outlier cap as E'[f - d + D] = Pair - cap (<= 0, exact integers in exact
   // mode): the DP kernel works with W-rows LUT_object[f][v] - cap * v.
@@ -282,6 +317,26 @@ int stixels_create(const stixels_params* params, int width, int height, int max_
   int band = 0;
   for (int d = -D; d <= D; ++d)
     if (E1[d + D] != 0.f) band = std::max(band, std::abs(d));
+  // NEXT f2: Pair[f][d] = Eq4(d - f, sigma_O(f)), a genuine D x D table
+  const bool pair2d = !sig_o.empty();
+  std::vector<float> E2, WT;
+  if (pair2d) {
+    band = 0;
+    E2.assign((size_t)(D + 2) * DPv, 0.f);          // rows d = 0..D (pixel), D+1 invalid
+    for (int d = 0; d <= D; ++d)
+      for (int f = 0; f < D; ++f) {
+        const double x = hm.Q(hm.eq4((double)(d - f), sig_o[f])) - capQ;
+        E2[(size_t)d * DPv + f] = (float)x;
+        if (x != 0.0) band = std::max(band, std::abs(d - f));
+      }
+    if (band > 7) return bail(STIXELS_ERR_UNSUPPORTED, "sigma_object_f: the pair-cost band exceeds 7 disparities");
+    WT.assign((size_t)(DPv + 17) * 16, 0.f);        // [wt_rows<DP>()][16]
+    for (int d = 0; d <= D; ++d)                    // row drp = d + 1, lane offset o = f - d + 7
+      for (int o = 0; o < 15; ++o) {
+        const int f = d + o - 7;
+        if (f >= 0 && f < D) WT[(size_t)(d + 1) * 16 + o] = -E2[(size_t)d * DPv + f];
+      }
+  }
   const bool sparse = band <= 7;
   // magic reciprocals: floor(y/(2n)) = umulhi(y, ceil(2^31/n))
   std::vector<uint32_t> M2(height + 1);
@@ -307,7 +362,7 @@ int stixels_create(const stixels_params* params, int width, int height, int max_
     A.thrB[v] = (int)bb;
     thrg[v] = (uint32_t)a1 | ((uint32_t)bb << 16);
   }
-  for (int d = -7; d <= 7; ++d) A.wt[d + 7] = sparse ? -E1[d + D] : 0.f;
+  for (int d = -7; d <= 7; ++d) A.wt[d + 7] = (sparse && !pair2d) ? -E1[d + D] : 0.f;
   A.wt[15] = 0.f;
   // priors (L#1): each constant quantized on its own
   const double bic = Host::nl(params->p_exist);
@@ -348,8 +403,9 @@ int stixels_create(const stixels_params* params, int width, int height, int max_
                   "exact mode range: h*cap + priors >= 2^24 quanta; lower cost_frac_bits (L#22)");
   }
   h->sparse = sparse;
+  h->pair2d = pair2d;
   A.h = height; A.D = D; A.n_cols = h->n_cols; A.cap = h->cap;
-  A.LG = (int)gG.size(); A.LS = (int)gS.size(); A.esz = esz; A.dmr_inv = einv;
+  A.LG = LGr; A.gG_stride = sig_g.empty() ? 0 : LGr; A.LS = (int)gS.size(); A.esz = esz; A.dmr_inv = einv;
   A.ord_margin = params->ord_margin;
   A.capQ = (float)capQ;
   A.cost_scale = params->cost_frac_bits > 0 ? (float)std::ldexp(1.0, -params->cost_frac_bits) : 1.f;
@@ -364,13 +420,17 @@ int stixels_create(const stixels_params* params, int width, int height, int max_
   h->sms = prop.multiProcessorCount;
   int optin = (int)prop.sharedMemPerBlockOptin;
   auto kfun = [&]() -> const void* {
-    if (DPv == 128) return sparse ? (const void*)dp_kernel<128, true> : (const void*)dp_kernel<128, false>;
-    return sparse ? (const void*)dp_kernel<256, true> : (const void*)dp_kernel<256, false>;
+    if (DPv == 128)
+      return pair2d ? (const void*)dp_kernel<128, true, true>
+                    : sparse ? (const void*)dp_kernel<128, true, false> : (const void*)dp_kernel<128, false, false>;
+    return pair2d ? (const void*)dp_kernel<256, true, true>
+                  : sparse ? (const void*)dp_kernel<256, true, false> : (const void*)dp_kernel<256, false, false>;
   };
   int cb = DPv == 128 ? (sparse ? col_smem_bytes<128, true>(height) : col_smem_bytes<128, false>(height))
                       : (sparse ? col_smem_bytes<256, true>(height) : col_smem_bytes<256, false>(height));
   int sb = stx::kM2Pad + al16((height + 1) * 4) + (sparse ? stx::e_copies<true>() : stx::e_copies<false>()) * esz * 4 +
-           al16(kTri * 2);   // pad, M2, E copies, triangle decode
+           al16(kTri * 2) +   // pad, M2, E copies, triangle decode
+           (pair2d ? (DPv + 17) * 16 * 4 : 0);   // NEXT f2 band weights
   int cpc = std::min(4, (optin - sb) / cb);   // columns per CTA (4 warps each)
   if (cpc < 1) return bail(STIXELS_ERR_UNSUPPORTED, "per-column shared memory exceeds the SM");
   h->cols_per_cta = cpc;
@@ -387,6 +447,13 @@ int stixels_create(const stixels_params* params, int width, int height, int max_
   h->red_smem = kRedRows * (h->red_tc * params->stixel_width + 1) * 2;
 
   auto alloc = [&](void** ptr, size_t n) { return cudaMalloc(ptr, n); };
+  if (pair2d && ((e = alloc((void**)&h->d_E2, E2.size() * 4)) != cudaSuccess ||
+                  (e = alloc((void**)&h->d_WT, WT.size() * 4)) != cudaSuccess))
+    return bail(STIXELS_ERR_CUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+  if (pair2d) {
+    cudaMemcpy(h->d_E2, E2.data(), E2.size() * 4, cudaMemcpyHostToDevice);
+    cudaMemcpy(h->d_WT, WT.data(), WT.size() * 4, cudaMemcpyHostToDevice);
+  }
   if ((e = alloc((void**)&h->d_E, E4.size() * 4)) != cudaSuccess ||
       (e = alloc((void**)&h->d_M2, M2.size() * 4)) != cudaSuccess ||
       (e = alloc((void**)&h->d_gG, gG.size() * 4)) != cudaSuccess ||
@@ -407,7 +474,7 @@ int stixels_create(const stixels_params* params, int width, int height, int max_
   cudaMemset(h->d_overflow, 0, 4);
   e = cudaDeviceSynchronize();
   if (e != cudaSuccess) return bail(STIXELS_ERR_CUDA, std::string("table upload: ") + cudaGetErrorString(e));
-  A.E = h->d_E; A.M2 = h->d_M2; A.gG = h->d_gG; A.gS = h->d_gS; A.dgR = h->d_dgR; A.thrg = h->d_thr;
+  A.E = h->d_E; A.E2g = h->d_E2; A.WTg = h->d_WT; A.M2 = h->d_M2; A.gG = h->d_gG; A.gS = h->d_gS; A.dgR = h->d_dgR; A.thrg = h->d_thr;
   A.overflow = h->d_overflow;
   A.scratch = h->d_scratch;
   *out = h;
@@ -445,11 +512,13 @@ static int launch_dp(stixels_handle* h, const uint16_t* d_cols, int batch, stixe
   int grid = std::min(h->grid, (A.items + h->cols_per_cta - 1) / h->cols_per_cta);
   const int threads = h->cols_per_cta * kCW * 32;
   if (h->dp_slots == 128) {
-    if (h->sparse) dp_kernel<128, true><<<grid, threads, h->smem, s>>>(A);
-    else dp_kernel<128, false><<<grid, threads, h->smem, s>>>(A);
+    if (h->pair2d) dp_kernel<128, true, true><<<grid, threads, h->smem, s>>>(A);
+    else if (h->sparse) dp_kernel<128, true, false><<<grid, threads, h->smem, s>>>(A);
+    else dp_kernel<128, false, false><<<grid, threads, h->smem, s>>>(A);
   } else {
-    if (h->sparse) dp_kernel<256, true><<<grid, threads, h->smem, s>>>(A);
-    else dp_kernel<256, false><<<grid, threads, h->smem, s>>>(A);
+    if (h->pair2d) dp_kernel<256, true, true><<<grid, threads, h->smem, s>>>(A);
+    else if (h->sparse) dp_kernel<256, true, false><<<grid, threads, h->smem, s>>>(A);
+    else dp_kernel<256, false, false><<<grid, threads, h->smem, s>>>(A);
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(h, STIXELS_ERR_CUDA, std::string("dp_kernel: ") + cudaGetErrorString(e));

@@ -151,12 +151,17 @@ struct DPArgs {
   float* scratch;          // [grid*cols_per_cta][2][h+1]  ground / sky prefix sums
   const float* E;          // [4][esz] object pair-cost windows (host built; sparse mode loads copy 0)
   const uint32_t* M2;      // [h+1] magic reciprocals ceil(2^31/n)
-  const float* gG;         // ground cost by |dR - dgR|, length LG (last = cap)
+  const float* gG;         // ground cost by |dR - dgR|, length LG (last = cap); with a
+                           // row-dependent sigma_G(v) (NEXT f2) one table per row v at
+                           // gG + v * gG_stride (gG_stride = 0: one shared table)
+  const float* E2g;        // NEXT f2, sigma_O(f): [D+2][DP] rows E'[d][f] = Pair[f][d] - cap
+                           // for pixel disparity d = 0..D, row D+1 = 0 (invalid pixel)
+  const float* WTg;        // NEXT f2: [DP+17][16] band weights cap - Pair[d+o-7][d] at row d+1
   const float* gS;         // sky cost by dR, length LS (last = cap)
   const int* dgR;          // [h] ground model, 1/256 units
   const uint32_t* thrg;    // [h] thrA1 | thrB << 16 (global copy for divergent reads)
   int* overflow;
-  int h, D, n_cols, items, cap, LG, LS, esz, dmr_inv, ord_margin, cols_per_cta;
+  int h, D, n_cols, items, cap, LG, LS, esz, dmr_inv, ord_margin, cols_per_cta, gG_stride;
   int col_bytes, shared_bytes;   // smem layout
   float capQ, cost_scale;
   float piFirstO, piFirstG;      // first-stixel priors (incl. BIC)
@@ -361,7 +366,14 @@ __device__ __forceinline__ void fadd2_inplace(float& a0, float& a1, float b0, fl
 // constant -cap*j is folded into the bottom's record.  All values stay exact
 // integers in exact mode (|.| <= 2 h cap < 2^24, checked on the host).
 // ---------------------------------------------------------------------------
-template <int DP, bool SPARSE>
+// NEXT f2 (PAIR2D): the object noise depends on the object's disparity f,
+// sigma_O(f), so Pair[f][d] is a genuine 2-D table: the W-row
+// band weights come from a [drp][offset] table in shared memory and the block
+// W-rows from the full [d][f] table in global memory (L2-resident).
+template <int DP>
+__host__ __device__ constexpr int wt_rows() { return DP + 17; }   // drp 0 .. no_band()
+
+template <int DP, bool SPARSE, bool PAIR2D>
 __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_constant__ DPArgs a) {
   constexpr int NR = DP / 128;         // LDS.128 ring windows per lane
   constexpr int NS = DP / 32;          // 32-wide f slices
@@ -399,6 +411,9 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
   uint16_t* tri_jk = reinterpret_cast<uint16_t*>(smem + kM2Pad + al16((h + 1) * 4) + e_copies<SPARSE>() * a.esz * 4);
   for (int i = threadIdx.x; i <= h; i += blockDim.x) M2s[i] = a.M2[i];
   for (int i = threadIdx.x; i < e_copies<SPARSE>() * a.esz; i += blockDim.x) E[i] = a.E[i];
+  float* WT = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(tri_jk) + al16(kTri * 2));
+  if constexpr (PAIR2D)
+    for (int i = threadIdx.x; i < wt_rows<DP>() * 16; i += blockDim.x) WT[i] = a.WTg[i];
   for (int jp = 0; jp < 31; ++jp)                 // triangle cell index -> (j', k')
     for (int kp = jp + 1 + (int)threadIdx.x; kp < 32; kp += blockDim.x)
       tri_jk[tri_off(jp) + kp - jp - 1] = (uint16_t)(jp | (kp << 8));
@@ -422,6 +437,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
   // lanes 15/31 sit out (a loop-invariant predicate): with them each half-warp
   // would span 16 banks and the two halves would collide whenever their f differ
   const bool blive = (lane & 15) < 15;
+  const uint32_t wt_s = (uint32_t)__cvta_generic_to_shared(WT) + (lane & 15) * 4u;   // PAIR2D
   // dead lanes (lane 15/31, zero weight) get an offset that puts every f out of range
   // ---- helpers --------------------------------------------------------------
   // dense W-row step: rr += E'[.][d_src] for f = 4*lane.. (+128 r); store to slot
@@ -459,7 +475,12 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
     auto band = [&](int drpA, int drpB) {
       const int drp = (lane < 16) ? drpA : drpB;
       float* q = shp<float>(bbuf_s + 4u * (uint32_t)drp);
-      if (blive) *q -= bwt;
+      if constexpr (PAIR2D) {
+        const float wgt = *shp<const float>(wt_s + 64u * (uint32_t)drp);
+        if (blive) *q -= wgt;
+      } else {
+        if (blive) *q -= bwt;
+      }
     };
     auto rowj = [&](int j) {
       const uint4* q = shp<const uint4>(rec_s + 32u * (uint32_t)j);
@@ -570,7 +591,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
       if (v < h) {
         float xg = capQ, xs = capQ;
         if (valid) {
-          xg = __ldg(a.gG + min(abs(dR - __ldg(a.dgR + v)), a.LG - 1));
+          xg = __ldg(a.gG + v * a.gG_stride + min(abs(dR - __ldg(a.dgR + v)), a.LG - 1));
           xs = __ldg(a.gS + min(dR, a.LS - 1));
         }
         tG[v] = xg; tS[v] = xs;
@@ -586,7 +607,10 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
       // E offsets of this row
       int dmr = valid ? a.D - dr : a.dmr_inv;
       int cc = dmr & 3;
-      cs.eo[v] = (uint32_t)(cc * a.esz * 4 + (dmr - cc) * 4) | ((uint32_t)(dmr * 4) << 16);
+      // hi16: E' row of the build -- the byte offset of its window in E copy 0, or
+      // (PAIR2D) the row index d of the 2-D table (D + 1 = invalid)
+      const uint32_t ehi = PAIR2D ? (uint32_t)(valid ? dr : a.D + 1) : (uint32_t)(dmr * 4);
+      cs.eo[v] = (uint32_t)(cc * a.esz * 4 + (dmr - cc) * 4) | (ehi << 16);
     }
     for (int i = ctid; i < DP; i += kCW * 32) ANg[i] = 0.f;   // W[.][0] = 0
     if (ctid == 0) *cs.ctr = 0;
@@ -642,7 +666,10 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
           for (int r = 0; r < 8; ++r) {
             const uint32_t e = __shfl_sync(0xffffffffu, eor, i0 + r);
 #pragma unroll
-            for (int c = 0; c < NS; ++c) x[r][c] = *shp<const float>(src_s + e + 128u * c);
+            for (int c = 0; c < NS; ++c) {
+              if constexpr (PAIR2D) x[r][c] = __ldg(a.E2g + e * DP + 32 * c + lane);
+              else x[r][c] = *shp<const float>(src_s + e + 128u * c);
+            }
           }
 #pragma unroll
           for (int r = 0; r < 8; ++r) {

@@ -42,6 +42,8 @@ class Params(ctypes.Structure):
         ("disp_format", ctypes.c_int32), ("disp_frac_bits", ctypes.c_int32),
         ("invalid_value", ctypes.c_uint32), ("reduce_mode", ctypes.c_int32),
         ("cost_frac_bits", ctypes.c_int32), ("max_stixels", ctypes.c_int32),
+        ("sigma_object_f", ctypes.POINTER(ctypes.c_float)),    # NEXT f2 (NULL = constant)
+        ("sigma_ground_v", ctypes.POINTER(ctypes.c_float)),
     ]
 
 
@@ -112,6 +114,14 @@ def params_from_dict(d: dict, H: int) -> Params:
     p.cost_frac_bits = int(d["cost_frac_bits"])
     p.max_stixels = int(d.get("max_stixels", 0))
     p.reduce_mode = int(d.get("reduce_mode", REDUCE_MEAN))
+    # NEXT f2 noise-model tables: the float32 arrays are kept alive on the struct
+    # (stixels_create copies them)
+    for key, n in (("sigma_object_f", p.max_disparity), ("sigma_ground_v", H)):
+        if d.get(key) is not None:
+            arr = np.ascontiguousarray(np.asarray(d[key], dtype=np.float32))
+            assert arr.shape == (n,), (key, arr.shape, n)
+            setattr(p, "_keep_" + key, arr)
+            setattr(p, key, arr.ctypes.data_as(ctypes.POINTER(ctypes.c_float)))
     return p
 
 

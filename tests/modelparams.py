@@ -59,4 +59,8 @@ def oracle_model(p, H):
         p_trans=np.array([[f32(x) for x in row] for row in np.asarray(p["p_trans"])]),
         p_ord=f32(p["p_ord"]), p_grav=f32(p["p_grav"]), p_blg=f32(p["p_blg"]),
         p_exist=f32(p["p_exist"]), ord_margin=p["ord_margin"], grav_margin=p["grav_margin"],
-        alpha=alpha, horizon_row=hz)
+        alpha=alpha, horizon_row=hz,
+        sigma_o_f=None if p.get("sigma_object_f") is None
+        else np.asarray(p["sigma_object_f"], np.float32).astype(np.float64),
+        sigma_g_v=None if p.get("sigma_ground_v") is None
+        else np.asarray(p["sigma_ground_v"], np.float32).astype(np.float64))

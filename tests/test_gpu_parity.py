@@ -74,6 +74,44 @@ def test_median_mode_end_to_end_exact():
     _assert_exact(p, frames)
 
 
+def _sigma_tables(seed, D, H):
+    rng = np.random.default_rng(seed)
+    f = np.arange(D)
+    so = 0.7 + 1.4 / (1.0 + np.exp(-(f - D / 2) / (D / 10)))        # a sigmoid in f
+    so = (so * rng.uniform(0.9, 1.1, D)).astype(np.float32)
+    sg = rng.uniform(0.8, 3.0, H).astype(np.float32)
+    return so, sg
+
+
+def test_noise_model_tables_exact():
+    """NEXT f2: sigma_O(f) (2-D pair table) and sigma_G(v) (per-row ground
+    tables): identical lists and costs on C2 frames."""
+    frames = _frames_c2(2, seed0=2700)
+    so, sg = _sigma_tables(1, 128, 440)
+    p = mp.make(sigma_object_f=so, sigma_ground_v=sg)
+    _assert_exact(p, frames)
+
+
+@pytest.mark.parametrize("H,W,D", [(33, 61, 128), (100, 70, 256), (65, 96, 200)])
+def test_noise_model_tables_shapes_exact(H, W, D):
+    so, sg = _sigma_tables(H + D, D, H)
+    frames = np.stack([synth.uniform_random_image(55, W, H, D),
+                       synth.render(synth.random_scene(56, W, H, D, alpha=0.9 * D / H), 56)])
+    p = mp.make(max_disparity=D, ground_slope=0.9 * D / H, sigma_object_f=so, sigma_ground_v=sg)
+    _assert_exact(p, frames)
+
+
+def test_constant_noise_tables_equal_scalar_model():
+    """Tables filled with the class constants give the scalar model's bytes."""
+    frames = _frames_c2(1, seed0=2800)
+    p0 = mp.make()
+    p1 = mp.make(sigma_object_f=np.full(128, 1.0, np.float32),
+                 sigma_ground_v=np.full(440, 2.0, np.float32))
+    a = run_gpu(p0, frames)
+    b = run_gpu(p1, frames)
+    assert a[0] == b[0] and (a[1] == b[1]).all()
+
+
 def test_c1_scene_exact():
     sc = synth.c1_scene()
     frames = np.stack([synth.render(sc, 1, noise=False), synth.render(sc, 2)])

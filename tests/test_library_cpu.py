@@ -2,6 +2,8 @@
 every symbol include/stixels.h declares, and validates parameters (the host
 checks run before any device call, so they are testable without a GPU)."""
 import ctypes
+
+import numpy as np
 import os
 import re
 import subprocess
@@ -49,7 +51,7 @@ def test_library_is_sm100a_only():
 
 
 def test_struct_layout_matches_header():
-    assert ctypes.sizeof(S.Params) == 4 * (6 + 1 + 3 + 1 + 3 + 9 + 4 + 2 + 2 + 4 + 2)
+    assert ctypes.sizeof(S.Params) == 4 * (6 + 1 + 3 + 1 + 3 + 9 + 4 + 2 + 2 + 4 + 2) + 4 + 2 * 8
     assert S.STIXEL_DTYPE.itemsize == 12
 
 
@@ -90,6 +92,21 @@ def test_median_width_limit():
     p.reduce_mode = S.REDUCE_MEDIAN
     p.stixel_width = 65
     assert _create(p, W=1040) == S.ERR_UNSUPPORTED
+
+
+def test_sigma_tables_validated():
+    """NEXT f2 tables: entries must be finite and > 0; an object band wider than
+    7 disparities is unsupported (checked before any device work)."""
+    from tests import modelparams as mp
+    D, H = 64, 120
+    bad = np.full(D, 1.0, np.float32)
+    bad[5] = 0.0
+    assert _create(S.params_from_dict(mp.make(max_disparity=D, sigma_object_f=bad), H), H=H) == S.ERR_PARAM
+    wide = np.full(D, 4.0, np.float32)
+    assert _create(S.params_from_dict(mp.make(max_disparity=D, sigma_object_f=wide), H), H=H) == S.ERR_UNSUPPORTED
+    g = np.full(H, 1.0, np.float32)
+    g[-1] = np.nan
+    assert _create(S.params_from_dict(mp.make(max_disparity=D, sigma_ground_v=g), H), H=H) == S.ERR_PARAM
 
 
 def test_exact_mode_range_guard():
