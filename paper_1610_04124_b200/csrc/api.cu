@@ -318,7 +318,9 @@ int stixels_create(const stixels_params* params, int width, int height, int max_
   for (int d = -D; d <= D; ++d)
     if (E1[d + D] != 0.f) band = std::max(band, std::abs(d));
   // NEXT f2: Pair[f][d] = Eq4(d - f, sigma_O(f)), a genuine D x D table
-  const bool pair2d = !sig_o.empty();
+  // any noise table selects the PAIR2D kernel; a missing sigma_O(f) table is the constant
+  const bool pair2d = !sig_o.empty() || !sig_g.empty();
+  if (pair2d && sig_o.empty()) sig_o.assign(D, (double)params->sigma[1]);
   std::vector<float> E2, WT;
   if (pair2d) {
     band = 0;
@@ -495,10 +497,10 @@ static int launch_reduce(stixels_handle* h, const void* d_disp, int64_t pitch, i
   r.s = h->p.stixel_width; r.tc = h->red_tc; r.q_bits = h->p.disp_frac_bits; r.D = h->p.max_disparity;
   r.bpp = h->p.disp_format == STIXELS_U16 ? 2 : 1;
   r.invalid = h->p.invalid_value;
-  r.median = h->p.reduce_mode == STIXELS_REDUCE_MEDIAN;
   r.out = d_cols;
   dim3 grid((h->n_cols + h->red_tc - 1) / h->red_tc, (h->H + kRedRows - 1) / kRedRows, batch);
-  reduce_kernel<<<grid, kRedThreads, h->red_smem, s>>>(r);
+  if (h->p.reduce_mode == STIXELS_REDUCE_MEDIAN) reduce_kernel<true><<<grid, kRedThreads, h->red_smem, s>>>(r);
+  else reduce_kernel<false><<<grid, kRedThreads, h->red_smem, s>>>(r);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(h, STIXELS_ERR_CUDA, std::string("reduce_kernel: ") + cudaGetErrorString(e));
   return STIXELS_OK;

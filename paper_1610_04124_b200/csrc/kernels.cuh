@@ -42,11 +42,11 @@ struct ReduceArgs {
   int64_t pitch;        // bytes
   int W, H, n_cols, s, tc, q_bits, D, bpp;
   uint32_t invalid;
-  int median;           // 0: mean of the valid pixels; 1: their median (f4)
   uint16_t* out;        // [batch][n_cols][H], 0xFFFF = invalid
 };
 constexpr int kMedianMaxS = 64;
 
+template <bool MEDIAN>
 __global__ void __launch_bounds__(kRedThreads) reduce_kernel(ReduceArgs a) {
   extern __shared__ uint16_t tile[];             // [kRedRows][tpx + 1]
   const int frame = blockIdx.z;
@@ -83,7 +83,7 @@ __global__ void __launch_bounds__(kRedThreads) reduce_kernel(ReduceArgs a) {
       sum += ok ? u : 0u;
       n += ok ? 1u : 0u;
     }
-    if (a.median && n) {
+    if (MEDIAN && n) {
       // median of the n valid values (L#24): the values of ranks (n-1)/2 and n/2
       // by rank counting (s <= 64, no sort), averaged with the mean's rounding
       const uint32_t k1 = (n - 1) >> 1, k2 = n >> 1;
@@ -154,14 +154,11 @@ struct DPArgs {
   const float* gG;         // ground cost by |dR - dgR|, length LG (last = cap); with a
                            // row-dependent sigma_G(v) (NEXT f2) one table per row v at
                            // gG + v * gG_stride (gG_stride = 0: one shared table)
-  const float* E2g;        // NEXT f2, sigma_O(f): [D+2][DP] rows E'[d][f] = Pair[f][d] - cap
-                           // for pixel disparity d = 0..D, row D+1 = 0 (invalid pixel)
-  const float* WTg;        // NEXT f2: [DP+17][16] band weights cap - Pair[d+o-7][d] at row d+1
   const float* gS;         // sky cost by dR, length LS (last = cap)
   const int* dgR;          // [h] ground model, 1/256 units
   const uint32_t* thrg;    // [h] thrA1 | thrB << 16 (global copy for divergent reads)
   int* overflow;
-  int h, D, n_cols, items, cap, LG, LS, esz, dmr_inv, ord_margin, cols_per_cta, gG_stride;
+  int h, D, n_cols, items, cap, LG, LS, esz, dmr_inv, ord_margin, cols_per_cta;
   int col_bytes, shared_bytes;   // smem layout
   float capQ, cost_scale;
   float piFirstO, piFirstG;      // first-stixel priors (incl. BIC)
@@ -171,6 +168,11 @@ struct DPArgs {
   float wt[16];                  // sparse W-row update: cap - Pair(d) for d = -7..7
   int thrA1[kMaxH];              // per row j: f >= thrA1[j] <=> floating object at base j
   int thrB[kMaxH];               //            f <  thrB[j]  <=> object below ground at base j
+  // NEXT f2 tables (PAIR2D instantiation only)
+  const float* E2g;        // NEXT f2, sigma_O(f): [D+2][DP] rows E'[d][f] = Pair[f][d] - cap
+                           // for pixel disparity d = 0..D, row D+1 = 0 (invalid pixel)
+  const float* WTg;        // NEXT f2: [DP+17][16] band weights cap - Pair[d+o-7][d] at row d+1
+  int gG_stride;
 };
 
 struct ColSmem {
@@ -366,10 +368,12 @@ __device__ __forceinline__ void fadd2_inplace(float& a0, float& a1, float b0, fl
 // constant -cap*j is folded into the bottom's record.  All values stay exact
 // integers in exact mode (|.| <= 2 h cap < 2^24, checked on the host).
 // ---------------------------------------------------------------------------
-// NEXT f2 (PAIR2D): the object noise depends on the object's disparity f,
-// sigma_O(f), so Pair[f][d] is a genuine 2-D table: the W-row
-// band weights come from a [drp][offset] table in shared memory and the block
-// W-rows from the full [d][f] table in global memory (L2-resident).
+// NEXT f2 (PAIR2D, any noise table given): the object noise depends on the
+// object's disparity f, sigma_O(f), so Pair[f][d] is a genuine 2-D table
+// (P:175): the W-row band weights come from a [drp][offset] table in shared
+// memory and the block W-rows from the full [d][f] table in global memory
+// (L2-resident); the ground cost table is per row (sigma_G(v)).  The default
+// instantiation (PAIR2D = false) keeps the 1-D |f - d| form.
 template <int DP>
 __host__ __device__ constexpr int wt_rows() { return DP + 17; }   // drp 0 .. no_band()
 
@@ -437,7 +441,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
   // lanes 15/31 sit out (a loop-invariant predicate): with them each half-warp
   // would span 16 banks and the two halves would collide whenever their f differ
   const bool blive = (lane & 15) < 15;
-  const uint32_t wt_s = (uint32_t)__cvta_generic_to_shared(WT) + (lane & 15) * 4u;   // PAIR2D
+  const uint32_t wt_s = PAIR2D ? (uint32_t)__cvta_generic_to_shared(WT) + (lane & 15) * 4u : 0u;
   // dead lanes (lane 15/31, zero weight) get an offset that puts every f out of range
   // ---- helpers --------------------------------------------------------------
   // dense W-row step: rr += E'[.][d_src] for f = 4*lane.. (+128 r); store to slot
@@ -591,7 +595,8 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
       if (v < h) {
         float xg = capQ, xs = capQ;
         if (valid) {
-          xg = __ldg(a.gG + v * a.gG_stride + min(abs(dR - __ldg(a.dgR + v)), a.LG - 1));
+          const float* gGv = PAIR2D ? a.gG + v * a.gG_stride : a.gG;   // f2: per-row tables
+          xg = __ldg(gGv + min(abs(dR - __ldg(a.dgR + v)), a.LG - 1));
           xs = __ldg(a.gS + min(dR, a.LS - 1));
         }
         tG[v] = xg; tS[v] = xs;
