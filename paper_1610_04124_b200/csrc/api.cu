@@ -27,7 +27,7 @@ struct stixels_handle {
   int n_cols = 0, cap = 0, dp_slots = 128, cols_per_cta = 0, smem = 0, grid = 0, sms = 0;
   bool sparse = true;
   bool pair2d = false;          // NEXT f2: sigma_O(f) table given
-  int red_tc = 0, red_smem = 0;
+  int red_tc = 0, red_smem = 0, red_w2 = 0;
   DPArgs args{};
   float* d_E = nullptr;
   float* d_E2 = nullptr;        // NEXT f2: [D+2][DP] 2-D pair table
@@ -446,7 +446,8 @@ int stixels_create(const stixels_params* params, int width, int height, int max_
   h->grid = h->sms * per_sm;
   // reduction tile
   h->red_tc = std::max(1, std::min(h->n_cols, 512 / params->stixel_width));
-  h->red_smem = kRedRows * (h->red_tc * params->stixel_width + 1) * 2;
+  h->red_w2 = red_tile_words(h->red_tc, params->stixel_width, params->disp_format == STIXELS_U16 ? 2 : 1);
+  h->red_smem = kRedRows * h->red_w2 * 4;
 
   auto alloc = [&](void** ptr, size_t n) { return cudaMalloc(ptr, n); };
   if (pair2d && ((e = alloc((void**)&h->d_E2, E2.size() * 4)) != cudaSuccess ||
@@ -497,6 +498,8 @@ static int launch_reduce(stixels_handle* h, const void* d_disp, int64_t pitch, i
   r.s = h->p.stixel_width; r.tc = h->red_tc; r.q_bits = h->p.disp_frac_bits; r.D = h->p.max_disparity;
   r.bpp = h->p.disp_format == STIXELS_U16 ? 2 : 1;
   r.invalid = h->p.invalid_value;
+  r.w2 = h->red_w2;
+  r.vec = ((uintptr_t)d_disp % 16 == 0) && (pitch % 16 == 0);
   r.out = d_cols;
   dim3 grid((h->n_cols + h->red_tc - 1) / h->red_tc, (h->H + kRedRows - 1) / kRedRows, batch);
   if (h->p.reduce_mode == STIXELS_REDUCE_MEDIAN) reduce_kernel<true><<<grid, kRedThreads, h->red_smem, s>>>(r);

@@ -28,11 +28,13 @@ constexpr int kMaxH = 1024;
 constexpr int kStart = 3;       // start marker class (first stixel)
 
 // ---------------------------------------------------------------------------
-// K1: column reduction + transpose.
+// K1: column reduction + transpose (HBM-bound).
 // One CTA = a tile of kRedRows image rows x (tc reduced columns) of one frame.
-// Rows are read coalesced into shared memory; each thread then emits one
-// reduced value (c, v), consecutive threads -> consecutive v (coalesced,
-// transposed writes).
+// The rows' byte range is read with 16-byte vector loads (rounded out to 16-byte
+// boundaries) into a shared tile whose row stride is an odd number of words, so
+// the transposed reads below -- 32 threads on 32 rows of one column -- are
+// bank-conflict free.  Each thread then emits one reduced value (c, v),
+// consecutive threads -> consecutive v (coalesced transposed writes).
 // ---------------------------------------------------------------------------
 constexpr int kRedRows = 32;
 constexpr int kRedThreads = 256;
@@ -41,45 +43,68 @@ struct ReduceArgs {
   const uint8_t* disp;
   int64_t pitch;        // bytes
   int W, H, n_cols, s, tc, q_bits, D, bpp;
+  int w2;               // tile row stride in 32-bit words (odd)
+  int vec;              // 16-byte loads allowed (base and pitch 16-byte aligned)
   uint32_t invalid;
   uint16_t* out;        // [batch][n_cols][H], 0xFFFF = invalid
 };
 constexpr int kMedianMaxS = 64;
 
+__host__ __device__ inline int red_tile_words(int tc, int s, int bpp) {
+  return (((tc * s * bpp + 32 + 15) / 16 * 16) / 4) | 1;   // odd word stride
+}
+
 template <bool MEDIAN>
 __global__ void __launch_bounds__(kRedThreads) reduce_kernel(ReduceArgs a) {
-  extern __shared__ uint16_t tile[];             // [kRedRows][tpx + 1]
+  extern __shared__ uint32_t tile32[];           // [kRedRows][w2] raw input bytes
   const int frame = blockIdx.z;
   const int r0 = blockIdx.y * kRedRows;
   const int c0 = blockIdx.x * a.tc;
   const int ncl = min(a.tc, a.n_cols - c0);
-  const int tpx = a.tc * a.s;                    // pixels per tile row
   const int px = ncl * a.s;
-  const int stride = tpx + 1;
   const int nrows = min(kRedRows, a.H - r0);
   const uint8_t* base = a.disp + (int64_t)frame * a.H * a.pitch + (int64_t)r0 * a.pitch;
-  if (a.bpp == 2) {
-    for (int i = threadIdx.x; i < nrows * px; i += kRedThreads) {
-      int r = i / px, x = i - r * px;
-      const uint16_t* row = reinterpret_cast<const uint16_t*>(base + (int64_t)r * a.pitch);
-      tile[r * stride + x] = __ldg(row + c0 * a.s + x);
+  const int b0 = c0 * a.s * a.bpp;                 // first byte of the tile in a row
+  int off;                                         // element offset of pixel c0*s in the tile
+  if (a.vec) {
+    const int bs = b0 & ~15;
+    const int be = (b0 + px * a.bpp + 15) & ~15;
+    const int nvec = (be - bs) >> 4;
+    off = (b0 - bs) / a.bpp;
+    const int t = threadIdx.x;
+    const int rstep = kRedThreads / nvec;
+    const int v = t % nvec;
+    for (int rr = t / nvec; rr < nrows && t < rstep * nvec; rr += rstep) {
+      const uint4 x = __ldg(reinterpret_cast<const uint4*>(base + (int64_t)rr * a.pitch + bs) + v);
+      uint32_t* d = tile32 + rr * a.w2 + 4 * v;
+      d[0] = x.x; d[1] = x.y; d[2] = x.z; d[3] = x.w;
     }
   } else {
+    off = 0;
     for (int i = threadIdx.x; i < nrows * px; i += kRedThreads) {
-      int r = i / px, x = i - r * px;
-      tile[r * stride + x] = __ldg(base + (int64_t)r * a.pitch + c0 * a.s + x);
+      const int r = i / px, x = i - r * px;
+      const uint8_t* row = base + (int64_t)r * a.pitch + b0;
+      if (a.bpp == 2)
+        reinterpret_cast<uint16_t*>(tile32)[r * 2 * a.w2 + x] = __ldg(reinterpret_cast<const uint16_t*>(row) + x);
+      else
+        reinterpret_cast<uint8_t*>(tile32)[r * 4 * a.w2 + x] = __ldg(row + x);
     }
   }
   __syncthreads();
   const uint32_t lim = (uint32_t)a.D << a.q_bits;
+  const int shift = kRBits + 1 - a.q_bits;
   for (int i = threadIdx.x; i < ncl * kRedRows; i += kRedThreads) {
-    int cl = i / kRedRows, rr = kRedRows - 1 - (i - cl * kRedRows);  // v ascending
+    const int cl = i / kRedRows, rr = kRedRows - 1 - (i - cl * kRedRows);  // v ascending
     if (rr >= nrows) continue;
-    const uint16_t* p = tile + rr * stride + cl * a.s;
+    const int e0 = off + cl * a.s;
+    auto px_at = [&](int x) -> uint32_t {
+      return a.bpp == 2 ? reinterpret_cast<const uint16_t*>(tile32)[rr * 2 * a.w2 + e0 + x]
+                        : reinterpret_cast<const uint8_t*>(tile32)[rr * 4 * a.w2 + e0 + x];
+    };
     uint32_t sum = 0, n = 0;
     for (int x = 0; x < a.s; ++x) {
-      uint32_t u = p[x];
-      bool ok = (u != a.invalid) && (u < lim);
+      const uint32_t u = px_at(x);
+      const bool ok = (u != a.invalid) && (u < lim);
       sum += ok ? u : 0u;
       n += ok ? 1u : 0u;
     }
@@ -89,11 +114,11 @@ __global__ void __launch_bounds__(kRedThreads) reduce_kernel(ReduceArgs a) {
       const uint32_t k1 = (n - 1) >> 1, k2 = n >> 1;
       uint32_t va = 0, vb = 0;
       for (int x = 0; x < a.s; ++x) {
-        const uint32_t u = p[x];
+        const uint32_t u = px_at(x);
         if (u == a.invalid || u >= lim) continue;
         uint32_t less = 0, leq = 0;
         for (int y = 0; y < a.s; ++y) {
-          const uint32_t t = p[y];
+          const uint32_t t = px_at(y);
           const bool ok = (t != a.invalid) && (t < lim);
           less += (ok && t < u) ? 1u : 0u;
           leq += (ok && t <= u) ? 1u : 0u;
@@ -106,12 +131,13 @@ __global__ void __launch_bounds__(kRedThreads) reduce_kernel(ReduceArgs a) {
     }
     uint16_t val = 0xFFFF;
     if (n) {
-      // round half up of 2^R*sum/(2^Q*n) = floor((sum*2^(R+1-Q) + n) / (2n))
-      uint64_t num = ((uint64_t)sum << (kRBits + 1 - a.q_bits)) + n;
-      val = (uint16_t)(num / (2ull * n));
+      // round half up of 2^R*sum/(2^Q*n) = floor((sum*2^(R+1-Q) + n) / (2n)); 32-bit
+      // when it cannot overflow (sum < 2^(31-shift))
+      if (sum < (1u << (31 - shift))) val = (uint16_t)(((sum << shift) + n) / (2u * n));
+      else val = (uint16_t)((((uint64_t)sum << shift) + n) / (2ull * n));
     }
-    int r = r0 + rr;
-    int v = a.H - 1 - r;
+    const int r = r0 + rr;
+    const int v = a.H - 1 - r;
     a.out[((int64_t)frame * a.n_cols + c0 + cl) * a.H + v] = val;
   }
 }

@@ -112,6 +112,41 @@ def test_constant_noise_tables_equal_scalar_model():
     assert a[0] == b[0] and (a[1] == b[1]).all()
 
 
+@pytest.mark.parametrize("W,s,fmt", [(1024, 3, "u16"), (1024, 7, "u16"), (1040, 5, "u8"),
+                                      (512, 10, "u8"), (64, 64, "u16")])
+def test_reduce_vector_path_bit_exact(W, s, fmt):
+    """16-byte-load path of reduce_kernel (pitch and base 16-byte aligned): ragged
+    tails (W mod s), tiles not aligned to 16 bytes, u8 and u16, mean and median."""
+    import torch
+    from oracle import oracle as orc
+    from paper_1610_04124_b200 import stixels as S
+    H, D = 70, 64
+    rng = np.random.default_rng(W + s)
+    if fmt == "u16":
+        f = rng.integers(0, (D + 2) * 16, size=(2, H, W)).astype(np.uint16)
+        f[rng.random(f.shape) < 0.1] = 0xFFFF
+        kw = dict(invalid_value=0xFFFF, disp_frac_bits=4)
+        dev = torch.from_numpy(f.view(np.int16)).cuda()
+        dt = torch.int16
+    else:
+        f = rng.integers(0, 256, size=(2, H, W)).astype(np.uint8)
+        kw = dict(invalid_value=255, disp_frac_bits=2, disp_format=S.U8)
+        dev = torch.from_numpy(f).cuda()
+        dt = torch.int16
+    for mode in (0, 1):
+        p = mp.make(max_disparity=D, stixel_width=s, reduce_mode=mode, **kw)
+        hd = S.Handle(S.params_from_dict(p, H), W, H, 2)
+        cols = torch.empty((2, hd.n_cols, H), dtype=dt, device="cuda")
+        hd.reduce(dev, cols)
+        hd.sync()
+        got = cols.cpu().numpy().view(np.uint16).astype(np.int32)
+        got[got == 0xFFFF] = -1
+        for b in range(2):
+            want = orc.reduce(f[b], s, kw["disp_frac_bits"], kw["invalid_value"], D, mode=mode)
+            assert (got[b] == want).all(), (mode, b)
+        hd.destroy()
+
+
 def test_c1_scene_exact():
     sc = synth.c1_scene()
     frames = np.stack([synth.render(sc, 1, noise=False), synth.render(sc, 2)])
