@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(kRedThreads) reduce_kernel(ReduceArgs a) {
 // for the NEXT block b+1 and while warp 0 works on block b, every cell whose
 // bottom j is already final: its 32 target rows, and bottoms j <= K0 in 32-row
 // chunks.  Only the newest chunk (bottoms of block b) waits for warp 0, and is
-// split three ways.  The serial warp also finalises each target: ground and
+// split two ways (warps 2-3 meanwhile precompute the next triangle).  The serial warp also finalises each target: ground and
 // sky running minima (their data term does not depend on the predecessor, so
 // GR^k = PG[k+1] + min_j (C_O[j-1] + t - PG[j])), the index table and
 // the 32-byte record of row k+1 that later rectangles read.
@@ -203,7 +203,7 @@ struct DPArgs {
 
 struct ColSmem {
   float* priv;      // [32][DP+1]     priv[i][f] = LUT_object[f][32b+i+1] of the block being built
-  float* seed;      // [2][3][DP]     LUT rows 32b+8, +16, +24 of block b (parity b & 1)
+  float* seed;      // [2][DP]        W-row 32b+16 of block b (parity b & 1)
   float* ring;      // [4][ring_stride] per-warp W-rows W_j = LUT_object[.][j] - cap*j (RR = 2 sparse, 4 dense)
   float* cbd;       // [496]          triangle cells (bottom K0+1+j', target K0+k' > j'), packed
   uint16_t* cbf;    // [496]          ... f | gravity level << 12
@@ -247,7 +247,7 @@ template <int DP, bool SPARSE>
 __host__ __device__ inline int col_smem_bytes(int h) {
   int b = 0;
   b += al16(32 * (DP + 1) * 4);
-  b += al16(6 * DP * 4);
+  b += al16(2 * DP * 4);
   b += al16(kCW * ring_stride<DP, SPARSE>() * 4);
   b += al16(kTri * 4) + al16(kTri * 2);
   b += al16((h + 3) * 32);
@@ -270,7 +270,7 @@ template <int DP, bool SPARSE>
 __device__ inline ColSmem carve(uint8_t* p, int h) {
   ColSmem w;
   w.priv = reinterpret_cast<float*>(p); p += al16(32 * (DP + 1) * 4);
-  w.seed = reinterpret_cast<float*>(p); p += al16(6 * DP * 4);
+  w.seed = reinterpret_cast<float*>(p); p += al16(2 * DP * 4);
   w.ring = reinterpret_cast<float*>(p); p += al16(kCW * ring_stride<DP, SPARSE>() * 4);
   w.cbd = reinterpret_cast<float*>(p); p += al16(kTri * 4);
   w.cbf = reinterpret_cast<uint16_t*>(p); p += al16(kTri * 2);
@@ -722,11 +722,11 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
     // bottoms' W-rows are the block's own priv rows: data term (absolute),
     // f, gravity level.  The 496 cells are spread densely over the column group.
     // Also keeps the W-rows K0+8, K0+16, K0+24 as seeds of block bt+1's newest chunk.
-    auto precompute_cells = [&](int bt) {
+    auto precompute_cells = [&](int bt, int t0, int nthr) {
       const int K0b = bt << 5;
       const int jn = min(K0b + 31, h - 1) - K0b;
       const int ncell = tri_off(jn);
-      for (int idx = ctid; idx < ncell; idx += kCW * 32) {
+      for (int idx = t0; idx < ncell; idx += nthr) {
         const uint32_t jk = tri_jk[idx];
         const int jp = jk & 0xff, kp = jk >> 8;
         const int k = K0b + kp;
@@ -741,9 +741,12 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
           cs.cbf[idx] = (uint16_t)(f | (lvl << 12));
         }
       }
-      if (w > 0 && K0b + 32 < h) {      // seeds (only needed if a next block exists)
-        float* sd = cs.seed + ((bt & 1) * 3 + w - 1) * DP;
-        const float* row = cs.priv + (8 * w - 1) * (DP + 1);
+    };
+    // seed of the second half of block bt's newest chunk: W-row K0 + 16 (priv row 15)
+    auto copy_seed = [&](int bt) {
+      if ((bt << 5) + 32 < h) {          // only needed if a next block exists
+        float* sd = cs.seed + (bt & 1) * DP;
+        const float* row = cs.priv + 15 * (DP + 1);
         for (int f = lane; f < DP; f += 32) sd[f] = row[f];
       }
     };
@@ -769,7 +772,8 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
         rargj = 0;
       }
       cs.part[w * 32 + lane] = make_float2(rbest, __int_as_float(rargj));
-      precompute_cells(0);
+      precompute_cells(0, ctid, kCW * 32);
+      if (w == 2) copy_seed(0);
     }
     named_bar(bar_col, kCW * 32);
 
@@ -953,13 +957,18 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
       }
       named_bar(bar_col, kCW * 32);
       if (has_next) {
-        // newest chunk (bottoms K0+1 .. K0+32, final after block b's triangle),
-        // 8 rows per warp, seeded from W-rows K0, K0+8, K0+16, K0+24
-        float rr[4 * NR];
-        load_seed(rr, (w == 0) ? ANg + b * DP : cs.seed + ((b & 1) * 3 + w - 1) * DP);
-        rect_run(rr, K0 + 1 + 8 * w, 8, ppn_s, Tn, N4n, rbest, rargj);
+        // newest chunk (bottoms K0+1 .. K0+32, final after block b's triangle):
+        // warps 0 and 1 take 16 rows each, seeded from W-rows K0 and K0+16, while
+        // warps 2 and 3 precompute block b+1's triangle cells
+        if (w < 2) {
+          float rr[4 * NR];
+          load_seed(rr, (w == 0) ? ANg + b * DP : cs.seed + (b & 1) * DP);
+          rect_run(rr, K0 + 1 + 16 * w, 16, ppn_s, Tn, N4n, rbest, rargj);
+        } else {
+          precompute_cells(bn, ctid - 64, 64);
+          if (w == 2) copy_seed(bn);
+        }
         cs.part[w * 32 + lane] = make_float2(rbest, __int_as_float(rargj));
-        precompute_cells(bn);
         if (ctid == 0) *cs.ctr = 0;
       }
       named_bar(bar_col, kCW * 32);
