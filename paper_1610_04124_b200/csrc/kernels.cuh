@@ -205,8 +205,10 @@ struct ColSmem {
   float* priv;      // [32][DP+1]     priv[i][f] = LUT_object[f][32b+i+1] of the block being built
   float* seed;      // [2][DP]        W-row 32b+16 of block b (parity b & 1)
   float* ring;      // [4][ring_stride] per-warp W-rows W_j = LUT_object[.][j] - cap*j (RR = 2 sparse, 4 dense)
-  float* cbd;       // [496]          triangle cells (bottom K0+1+j', target K0+k' > j'), packed
-  uint16_t* cbf;    // [496]          ... f | gravity level << 12
+  float* cbd;       // [496]          triangle cells (bottom K0+1+j', target K0+k' > j'), packed:
+                    //                object data term,
+  float* cbg;       // [496]          ... the same plus its O-above-G prior (gravity level),
+  uint16_t* cbf;    // [496]          ... and the object mean f
   uint4* rec;       // [h+3][2]       row j: {AO0,AO1,AGm,AGh} {AGl, T[j], N4[j], ordthr | drp<<16}
   uint2* tn;        // [h+1]          row j: {T[j], N4[j]} (compact copy for per-lane rows)
   uint32_t* eo;     // [h+2]          lo16: ring window byte offset; hi16: E0 byte offset
@@ -249,7 +251,7 @@ __host__ __device__ inline int col_smem_bytes(int h) {
   b += al16(32 * (DP + 1) * 4);
   b += al16(2 * DP * 4);
   b += al16(kCW * ring_stride<DP, SPARSE>() * 4);
-  b += al16(kTri * 4) + al16(kTri * 2);
+  b += 2 * al16(kTri * 4) + al16(kTri * 2);
   b += al16((h + 3) * 32);
   b += al16((h + 1) * 8);
   b += al16((h + 2) * 4);
@@ -273,6 +275,7 @@ __device__ inline ColSmem carve(uint8_t* p, int h) {
   w.seed = reinterpret_cast<float*>(p); p += al16(2 * DP * 4);
   w.ring = reinterpret_cast<float*>(p); p += al16(kCW * ring_stride<DP, SPARSE>() * 4);
   w.cbd = reinterpret_cast<float*>(p); p += al16(kTri * 4);
+  w.cbg = reinterpret_cast<float*>(p); p += al16(kTri * 4);
   w.cbf = reinterpret_cast<uint16_t*>(p); p += al16(kTri * 2);
   w.rec = reinterpret_cast<uint4*>(p); p += al16((h + 3) * 32);
   w.tn = reinterpret_cast<uint2*>(p); p += al16((h + 1) * 8);
@@ -308,16 +311,6 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x, int lane) {
 // (keeps selects between kernel-parameter constants branch-free): a shuffle
 // result is opaque to ptxas.
 __device__ __forceinline__ float opaque(float x) { return __shfl_sync(0xffffffffu, x, 0); }
-
-// Gravity penalty by level (0 mid, 1 floating, 2 below ground) as two selects.
-__device__ __forceinline__ float pen3(int lvl, float mid, float hi, float lo) {
-  float r;
-  asm("{\n\t.reg .pred p1, p2;\n\t.reg .f32 t;\n\t"
-      "setp.eq.s32 p1, %1, 1;\n\tsetp.eq.s32 p2, %1, 2;\n\t"
-      "selp.f32 t, %3, %2, p1;\n\tselp.f32 %0, %4, t, p2;\n\t}"
-      : "=f"(r) : "r"(lvl), "f"(mid), "f"(hi), "f"(lo));
-  return r;
-}
 
 __device__ __forceinline__ void named_bar(int id, int threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
@@ -736,9 +729,10 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
           int f = span_f(rk.x - ry.x, rk.y - ry.y, smem, Dm1);
           float data = (cs.priv[kp * (DP + 1) + f] - cs.priv[jp * (DP + 1) + f]) + capQ * (float)(kp - jp);
           const uint32_t th = __ldg(a.thrg + K0b + jp + 1);
-          int lvl = (f >= (int)(th & 0xffffu)) ? 1 : ((f < (int)(th >> 16)) ? 2 : 0);
+          const float pen = (f >= (int)(th & 0xffffu)) ? a.kGO_hi : ((f < (int)(th >> 16)) ? a.kGO_lo : a.kGO_mid);
           cs.cbd[idx] = data;
-          cs.cbf[idx] = (uint16_t)(f | (lvl << 12));
+          cs.cbg[idx] = data + pen;
+          cs.cbf[idx] = (uint16_t)f;
         }
       }
     };
@@ -824,7 +818,6 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
         cs.pgps[lane] = make_float4(kOG - pg0, pg1, 0.f, 0.f);
         __syncwarp();
         const float oh = opaque(a.kOO_hi), ol = opaque(a.kOO_lo);
-        const float gh = opaque(a.kGO_hi), gl = opaque(a.kGO_lo), gm = opaque(a.kGO_mid);
         const int om = a.ord_margin;
 
         // Chain state: C_O, C_G and the object mean of the last finalised target.
@@ -843,12 +836,13 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
           const int j = K0 + jp + 1;                    // bottom j; target j finalised
           const float4 q = cs.pgps[jp + 1];
           // diagonal cell (bottom j, target j), evaluated redundantly by all lanes
+          // (data + min(aO, aG) computed as min(data + aO, (data + pen) + C_G): the
+          // same value, exactly so in exact mode (integer quanta))
           const float dd = cs.cbd[off];
-          const int dfl = cs.cbf[off];
-          const int df = dfl & 0xfff, dl = dfl >> 12;
+          const float dg = cs.cbg[off];
+          const int df = cs.cbf[off];
           const float daO = prevCO + ((df > prevF + om) ? oh : ol);
-          const float daG = prevCG + pen3(dl, gm, gh, gl);
-          const float dc = dd + fminf(daO, daG);
+          const float dc = fminf(dd + daO, dg + prevCG);
           const bool take = dc < rB;
           const float COj = take ? dc : rB;
           const int Fj = take ? df : rF;
@@ -856,12 +850,12 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
           {
             const int idx = off + lane - jp - 1;        // (lanes <= jp read a dead slot)
             const float data = cs.cbd[idx];
-            const int fl = cs.cbf[idx];
-            const int f = fl & 0xfff, lvl = fl >> 12;
-            const float aO = prevCO + ((f > prevF + om) ? oh : ol);
-            const float aG = prevCG + pen3(lvl, gm, gh, gl);
-            const bool pg = aG <= aO;
-            const float cand = data + (pg ? aG : aO);
+            const float dgl = cs.cbg[idx];
+            const int f = cs.cbf[idx];
+            const float tO = data + (prevCO + ((f > prevF + om) ? oh : ol));
+            const float tG = dgl + prevCG;
+            const bool pg = tG <= tO;                   // == (aG <= aO): data added to both
+            const float cand = pg ? tG : tO;
             const bool upd = (lane > jp) && (cand < best);
             best = upd ? cand : best;
             argj = upd ? j : argj;
