@@ -120,8 +120,14 @@ long long orc_ground_R(const orc_model* m, int v) {
  * Input: raw fixed-point disparities with Q_bits fractional bits (a1); a pixel
  * is invalid if it equals `invalid` or decodes to >= D (L#23).
  * Output: out[c*H + v] = round_half_up(2^R_bits * sum / (2^Q_bits * n)) in
- * units of 1/2^R_bits, v = H-1-r (model row from the bottom), or -1 = invalid.
+ * units of 1/2^R_bits, v = H-1-r (model row from the bottom), or -1 = invalid,
+ * clamped to below D - 1/2 (L#27): the pair LUT of P:175 is D x D, so a
+ * pixel's integer disparity round_half_up(d') must lie in [0, D).
  * ------------------------------------------------------------------------ */
+static int clamp_reduced(long long x, int D, int R_bits) {
+  long long mx = ((long long)(D - 1) << R_bits) + (1LL << (R_bits - 1)) - 1;
+  return (int)(x < mx ? x : mx);
+}
 void orc_reduce(const void* img, int bytes_per_px, int W, int H, long long pitch_px, int s,
                 int Q_bits, unsigned int invalid, int D, int R_bits, int* out) {
   int n_cols = W / s;
@@ -146,7 +152,7 @@ void orc_reduce(const void* img, int bytes_per_px, int W, int H, long long pitch
         /* round half up of (2^R * sum) / (2^Q * n) = floor((2*2^R*sum + 2^Q*n) / (2*2^Q*n)) */
         long long num = 2 * (sum << R_bits) + (n << Q_bits);
         long long den = 2 * (n << Q_bits);
-        out[(long long)c * H + v] = (int)(num / den);
+        out[(long long)c * H + v] = clamp_reduced(num / den, D, R_bits);
       }
     }
   }
@@ -158,7 +164,8 @@ void orc_reduce(const void* img, int bytes_per_px, int W, int H, long long pitch
  * of the VALID pixels among the s of a row segment -- the middle value of the
  * sorted valid values, the mean of the two middle values when their count is
  * even -- in units of 1/2^R_bits, rounded half up exactly like the mean
- * (orc_reduce with the middle value(s) as the summands).  All invalid -> -1.
+ * (orc_reduce with the middle value(s) as the summands) and clamped the same
+ * way (L#27).  All invalid -> -1.
  * Written the plain way: collect, sort (qsort), pick.
  * ------------------------------------------------------------------------ */
 static int cmp_uint(const void* a, const void* b) {
@@ -194,7 +201,7 @@ void orc_reduce_median(const void* img, int bytes_per_px, int W, int H, long lon
       else { sum = (long long)vals[n / 2 - 1] + vals[n / 2]; cnt = 2; }
       long long num = 2 * (sum << R_bits) + (cnt << Q_bits);
       long long den = 2 * (cnt << Q_bits);
-      out[(long long)c * H + v] = (int)(num / den);
+      out[(long long)c * H + v] = clamp_reduced(num / den, D, R_bits);
     }
   }
   free(vals);

@@ -133,8 +133,11 @@ __global__ void __launch_bounds__(kRedThreads) reduce_kernel(ReduceArgs a) {
     if (n) {
       // round half up of 2^R*sum/(2^Q*n) = floor((sum*2^(R+1-Q) + n) / (2n)); 32-bit
       // when it cannot overflow (sum < 2^(31-shift))
-      if (sum < (1u << (31 - shift))) val = (uint16_t)(((sum << shift) + n) / (2u * n));
-      else val = (uint16_t)((((uint64_t)sum << shift) + n) / (2ull * n));
+      uint32_t q;
+      if (sum < (1u << (31 - shift))) q = ((sum << shift) + n) / (2u * n);
+      else q = (uint32_t)((((uint64_t)sum << shift) + n) / (2ull * n));
+      // below D - 1/2 (L#27): the pixel's integer disparity indexes the D x D LUT
+      val = (uint16_t)min(q, ((uint32_t)(a.D - 1) << kRBits) + (1u << (kRBits - 1)) - 1u);
     }
     const int r = r0 + rr;
     const int v = a.H - 1 - r;
@@ -320,12 +323,14 @@ constexpr int kM2Pad = 16;          // bytes of shared memory before the M2 tabl
 
 // Object model value f of span [j, k] from prefix differences:
 // f = floor(t / (256 n)), t = sum(d + 128) over valid pixels: the exact half-up
-// rounded mean (L#10), via a multiply-high by ceil(2^31/n) (exact for t < 2^28),
-// clamped to D-1.  n4 = 4n is the byte offset into M2 (kM2Pad bytes into dynamic smem).
+// rounded mean (L#10), via a multiply-high by ceil(2^31/n) (exact for t < 2^28).
+// No clamp is needed: every reduced value is below D - 1/2 (L#27), so is their
+// rounded mean.  n4 = 4n is the byte offset into M2 (kM2Pad bytes into dynamic smem).
 __device__ __forceinline__ int span_f(uint32_t t, uint32_t n4, const uint8_t* smem0, int Dm1) {
   uint32_t y = t >> (kRBits - 1);
   uint32_t M = *reinterpret_cast<const uint32_t*>(smem0 + kM2Pad + n4);
-  return min((int)__umulhi(y, M), Dm1);
+  (void)Dm1;
+  return (int)__umulhi(y, M);
 }
 
 __device__ __forceinline__ uint4 lds128(uint32_t addr) {
@@ -518,7 +523,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
     auto fmean = [&](const RowU& r) {
       const uint32_t n4 = N4k - r.N4;
       const uint32_t M = *shp<const uint32_t>(m2_s + n4);
-      return min((int)__umulhi((Tk - r.T) >> (kRBits - 1), M), Dm1);
+      return (int)__umulhi((Tk - r.T) >> (kRBits - 1), M);   // < D: inputs below D - 1/2 (L#27)
     };
     RowU r0 = rowj(j0), r1 = rowj(j0 + 1);
     if constexpr (SPARSE) {
@@ -607,7 +612,9 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
       int dR = -1;
       if (v < h) {
         uint32_t u = col[v];
-        dR = (u == 0xffffu) ? -1 : (int)u;
+        // (clamped below D - 1/2 as stixels_reduce does, L#27, so caller-made
+        // columns cannot push an object mean past the table)
+        dR = (u == 0xffffu) ? -1 : min((int)u, ((a.D - 1) << kRBits) + (1 << (kRBits - 1)) - 1);
       }
       const bool valid = dR >= 0;
       const int dr = valid ? (dR + (1 << (kRBits - 1))) >> kRBits : -1;   // round half up (L#9)

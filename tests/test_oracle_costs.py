@@ -102,6 +102,19 @@ def test_reduce_spec_examples():
             assert out.shape == (case["n_cols"], case["h"])
 
 
+def test_reduce_clamps_below_d_minus_half():
+    """L#27: the reduced disparity stays below D - 1/2, so its integer rounding
+    (the pair-LUT index, L#9) lies in [0, D) -- the D x D LUT of P:175."""
+    D = 64
+    for q, top in ((4, D * 16 - 1), (0, D - 1), (8, D * 256 - 1)):
+        row = np.array([[top] * 5, [top - (1 << q) // 2] * 5], np.uint16)
+        out = orc.reduce(row, 5, q, 0xFFFF, D)
+        assert out.max() <= (D - 1) * 256 + 127
+        assert ((out + 128) >> 8).max() <= D - 1
+    # untouched below the bound: 63.25 px -> 63.25 * 256
+    assert orc.reduce(np.array([[63 * 16 + 4] * 5], np.uint16), 5, 4, 0xFFFF, D)[0, 0] == 63 * 256 + 64
+
+
 def test_reduce_properties():
     rng = np.random.default_rng(3)
     inv = 0xFFFF
