@@ -31,16 +31,20 @@ def stale() -> bool:
     return any(os.path.getmtime(s) > t for s in SOURCES + [HEADER])
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not stale():
+def build(force: bool = False, verbose: bool = False, trace: bool = False) -> str:
+    """trace=True builds the diagnostic phase-timeline variant libstixels_trace.so
+    (-DSTX_TRACE; scripts/trace_phases.py), never loaded by the product."""
+    out = LIB if not trace else os.path.join(HERE, "libstixels_trace.so")
+    if not trace and not force and not stale():
         return LIB
-    cmd = [nvcc()] + NVCC_FLAGS + ["-o", LIB, os.path.join(CSRC, "api.cu")]
+    cmd = [nvcc()] + NVCC_FLAGS + (["-DSTX_TRACE"] if trace else []) + ["-o", out,
+                                                                        os.path.join(CSRC, "api.cu")]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError("nvcc failed:\n" + res.stdout + res.stderr)
     if verbose:
         print(res.stderr)
-    return LIB
+    return out
 
 
 if __name__ == "__main__":

@@ -484,6 +484,15 @@ int stixels_create(const stixels_params* params, int width, int height, int max_
   return STIXELS_OK;
 }
 
+#ifdef STX_TRACE
+// diagnostic build only: device buffer of 4*64*16 u64 for the phase timeline
+extern "C" int stixels_trace_buffer(stixels_handle* h, void* d_buf) {
+  if (!h) return STIXELS_ERR_ARG;
+  h->args.trace = (unsigned long long*)d_buf;
+  return STIXELS_OK;
+}
+#endif
+
 int stixels_query(const stixels_handle* h, int* n_cols, int* cap) {
   if (!h) return STIXELS_ERR_ARG;
   if (n_cols) *n_cols = h->n_cols;

@@ -172,6 +172,18 @@ __global__ void __launch_bounds__(kRedThreads) reduce_kernel(ReduceArgs a) {
 // ---------------------------------------------------------------------------
 constexpr int kCW = 4;                 // warps per column
 
+// Diagnostic phase timeline (build with -DSTX_TRACE; scripts/trace_phases.py):
+// CTA 0's column groups record clock64 stamps of their first column's phases.
+#ifdef STX_TRACE
+#define STX_STAMP(blk, slot)                                                             \
+  do {                                                                                   \
+    if (blockIdx.x == 0 && first_item && lane == 0 && (blk) < 64)                        \
+      a.trace[(cslot * 64 + (blk)) * 16 + (slot)] = clock64();                           \
+  } while (0)
+#else
+#define STX_STAMP(blk, slot) do { } while (0)
+#endif
+
 struct DPArgs {
   const uint16_t* cols;    // [items][h] reduced columns (model order), 0xFFFF invalid
   stixel_t* out;           // [items][cap]
@@ -202,11 +214,15 @@ struct DPArgs {
                            // for pixel disparity d = 0..D, row D+1 = 0 (invalid pixel)
   const float* WTg;        // NEXT f2: [DP+17][16] band weights cap - Pair[d+o-7][d] at row d+1
   int gG_stride;
+#ifdef STX_TRACE
+  unsigned long long* trace;     // diagnostic build only: [4 groups][64 blocks][16] clock64 stamps
+#endif
 };
 
 struct ColSmem {
   float* priv;      // [32][DP+1]     priv[i][f] = LUT_object[f][32b+i+1] of the block being built
-  float* seed;      // [2][DP]        W-row 32b+16 of block b (parity b & 1)
+  float* seed;      // [3][DP] W-row 32b of block b (slot b % 3: written by the build two
+                    // blocks ahead), then [2][DP] W-row 32b+16 (slot b & 1)
   float* ring;      // [4][ring_stride] per-warp W-rows W_j = LUT_object[.][j] - cap*j (RR = 2 sparse, 4 dense)
   float* cbd;       // [496]          triangle cells (bottom K0+1+j', target K0+k' > j'), packed:
                     //                object data term,
@@ -252,7 +268,7 @@ template <int DP, bool SPARSE>
 __host__ __device__ inline int col_smem_bytes(int h) {
   int b = 0;
   b += al16(32 * (DP + 1) * 4);
-  b += al16(2 * DP * 4);
+  b += al16(5 * DP * 4);
   b += al16(kCW * ring_stride<DP, SPARSE>() * 4);
   b += 2 * al16(kTri * 4) + al16(kTri * 2);
   b += al16((h + 3) * 32);
@@ -275,7 +291,7 @@ template <int DP, bool SPARSE>
 __device__ inline ColSmem carve(uint8_t* p, int h) {
   ColSmem w;
   w.priv = reinterpret_cast<float*>(p); p += al16(32 * (DP + 1) * 4);
-  w.seed = reinterpret_cast<float*>(p); p += al16(2 * DP * 4);
+  w.seed = reinterpret_cast<float*>(p); p += al16(5 * DP * 4);
   w.ring = reinterpret_cast<float*>(p); p += al16(kCW * ring_stride<DP, SPARSE>() * 4);
   w.cbd = reinterpret_cast<float*>(p); p += al16(kTri * 4);
   w.cbg = reinterpret_cast<float*>(p); p += al16(kTri * 4);
@@ -602,6 +618,8 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
 
   float fr[NS];                        // builder warp: W[f][32 bt] for f = lane + 32c
 
+  bool first_item = true;
+  (void)first_item;
   for (int item = slot_global; item < a.items; item += gridDim.x * a.cols_per_cta) {
     const uint16_t* col = a.cols + (int64_t)item * h;
     // ---------------- prologue A (all 4 warps): per-pixel costs (a3-a4) ----------
@@ -643,9 +661,10 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
       const uint32_t ehi = PAIR2D ? (uint32_t)(valid ? dr : a.D + 1) : (uint32_t)(dmr * 4);
       cs.eo[v] = (uint32_t)(cc * a.esz * 4 + (dmr - cc) * 4) | (ehi << 16);
     }
-    for (int i = ctid; i < DP; i += kCW * 32) ANg[i] = 0.f;   // W[.][0] = 0
+    for (int i = ctid; i < DP; i += kCW * 32) { ANg[i] = 0.f; cs.seed[i] = 0.f; }   // W[.][0] = 0
     if (ctid == 0) *cs.ctr = 0;
     named_bar(bar_col, kCW * 32);
+    STX_STAMP(63, w);                    // clock calibration (all warps just released)
 
     // ---------------- prologue B (4 warps): prefix sums --------------
     // warp 0: ground PG, warp 1: sky PS, warp 2: disparity T, warp 3: count N4
@@ -716,7 +735,10 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
         }
       }
 #pragma unroll
-      for (int c = 0; c < NS; ++c) ANg[(bt + 1) * DP + 32 * c + lane] = fr[c];
+      for (int c = 0; c < NS; ++c) {
+        ANg[(bt + 1) * DP + 32 * c + lane] = fr[c];
+        cs.seed[((bt + 1) % 3) * DP + 32 * c + lane] = fr[c];   // newest-chunk seed of block bt+1
+      }
     };
     // triangle cells of block bt: bottom K0+1+j', target K0+k' (k' > j'); their
     // bottoms' W-rows are the block's own priv rows: data term (absolute),
@@ -735,8 +757,9 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
           const uint2 rk = cs.tn[k + 1];
           int f = span_f(rk.x - ry.x, rk.y - ry.y, smem, Dm1);
           float data = (cs.priv[kp * (DP + 1) + f] - cs.priv[jp * (DP + 1) + f]) + capQ * (float)(kp - jp);
-          const uint32_t th = __ldg(a.thrg + K0b + jp + 1);
-          const float pen = (f >= (int)(th & 0xffffu)) ? a.kGO_hi : ((f < (int)(th >> 16)) ? a.kGO_lo : a.kGO_mid);
+          // thresholds from the constant bank: a warp's cells span one or two rows
+          const int jr = K0b + jp + 1;
+          const float pen = (f >= a.thrA1[jr]) ? a.kGO_hi : ((f < a.thrB[jr]) ? a.kGO_lo : a.kGO_mid);
           cs.cbd[idx] = data;
           cs.cbg[idx] = data + pen;
           cs.cbf[idx] = (uint16_t)f;
@@ -746,7 +769,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
     // seed of the second half of block bt's newest chunk: W-row K0 + 16 (priv row 15)
     auto copy_seed = [&](int bt) {
       if ((bt << 5) + 32 < h) {          // only needed if a next block exists
-        float* sd = cs.seed + (bt & 1) * DP;
+        float* sd = cs.seed + (3 + (bt & 1)) * DP;
         const float* row = cs.priv + 15 * (DP + 1);
         for (int f = lane; f < DP; f += 32) sd[f] = row[f];
       }
@@ -791,6 +814,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
       const int bn = b + 1;
       const int Kn = bn << 5;
       const bool has_next = bn < nb;
+      if (w == 0) STX_STAMP(b, 0);
       if (w == 0) {
         // ============ serial warp: block b's triangle and finalisation ============
         const int kk = k < h ? k : h - 1;
@@ -932,9 +956,11 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
           cs.argS[k] = (uint16_t)aS;
           cs.fpv[k] = (uint8_t)argf;
         }
+        STX_STAMP(b, 1);
         if (has_next) named_bar(bar_x, kCW * 32);   // block b+1's priv rows are ready
       } else if (has_next) {
         if (w == 1) build_priv(bn);      // block b's priv rows are no longer needed
+        if (w == 1) STX_STAMP(b, 2);
         named_bar(bar_rect, 3 * 32);
         asm volatile("bar.arrive %0, %1;" ::"r"(bar_x), "r"(kCW * 32) : "memory");
       }
@@ -956,14 +982,16 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
         // full chunks m <= b-1: their records (rows <= 32 b) were final before block b
         bulk_chunks(b, ppn_s, Tn, N4n, rbest, rargj);
       }
+      STX_STAMP(b, 3 + w);
       named_bar(bar_col, kCW * 32);
+      if (w == 0) STX_STAMP(b, 7);
       if (has_next) {
         // newest chunk (bottoms K0+1 .. K0+32, final after block b's triangle):
         // warps 0 and 1 take 16 rows each, seeded from W-rows K0 and K0+16, while
         // warps 2 and 3 precompute block b+1's triangle cells
         if (w < 2) {
           float rr[4 * NR];
-          load_seed(rr, (w == 0) ? ANg + b * DP : cs.seed + (b & 1) * DP);
+          load_seed(rr, cs.seed + (w == 0 ? b % 3 : 3 + (b & 1)) * DP);   // W-rows K0, K0+16
           rect_run(rr, K0 + 1 + 16 * w, 16, ppn_s, Tn, N4n, rbest, rargj);
         } else {
           precompute_cells(bn, ctid - 64, 64);
@@ -972,7 +1000,9 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
         cs.part[w * 32 + lane] = make_float2(rbest, __int_as_float(rargj));
         if (ctid == 0) *cs.ctr = 0;
       }
+      STX_STAMP(b, 8 + w);
       named_bar(bar_col, kCW * 32);
+      if (w == 0) STX_STAMP(b, 12);
     }
 
     // ---------------- backtracking + extraction (a7), warp 0 ------------
@@ -1026,6 +1056,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
       }
       __syncwarp();
     }
+    first_item = false;
     named_bar(bar_col, kCW * 32);
   }
 }

@@ -1,0 +1,63 @@
+#!/usr/bin/env python3
+"""Phase timeline of dp_kernel's first column per column group of CTA 0 (diagnostic
+build libstixels_trace.so, -DSTX_TRACE).  Prints, per 32-row block b, cycles
+relative to the block start: serial triangle done, build done, each warp's bulk
+end, the bar release, each warp's newest-chunk end, the block end.
+usage (GPU box): python scripts/trace_phases.py [batch]"""
+import ctypes
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_1610_04124_b200 import build as B          # noqa: E402
+from paper_1610_04124_b200 import stixels as S        # noqa: E402
+from inputs import synth                              # noqa: E402
+from tests import modelparams as mp                   # noqa: E402
+
+lib = ctypes.CDLL(B.build(trace=True))
+batch = int(sys.argv[1]) if len(sys.argv) > 1 else 2048
+W, H = 1024, 440
+p = S.params_from_dict(mp.make(), H)
+h = ctypes.c_void_p()
+assert lib.stixels_create(ctypes.byref(p), W, H, batch, 0, None, ctypes.byref(h)) == 0
+pool = np.stack([synth.frame(3, i, W, H, 128) for i in range(16)])
+disp = torch.from_numpy(pool.view(np.int16)).cuda()[torch.arange(batch) % 16]
+nc = W // 5
+out = torch.empty((batch, nc, H, 12), dtype=torch.uint8, device="cuda")
+cnt = torch.empty((batch, nc), dtype=torch.int32, device="cuda")
+tr = torch.zeros(4 * 64 * 16, dtype=torch.int64, device="cuda")
+lib.stixels_trace_buffer(h, ctypes.c_void_p(tr.data_ptr()))
+P = lambda t: ctypes.c_void_p(t.data_ptr())
+for _ in range(2):
+    assert lib.stixels_compute(h, P(disp), ctypes.c_int64(W * 2), batch, P(out), P(cnt), None) == 0
+torch.cuda.synchronize()
+t = tr.cpu().numpy().reshape(4, 64, 16).astype(np.int64)
+# per-warp clock offsets (warps of a group sit on different SM sub-partitions):
+# calibration stamps right after a common barrier, block slot 63, positions w
+owner = {1: 0, 2: 1, 3: 0, 4: 1, 5: 2, 6: 3, 7: 0, 8: 0, 9: 1, 10: 2, 11: 3, 12: 0}
+for g in range(4):
+    cal = t[g, 63, :4] - t[g, 63, 0]
+    print(f"group {g}: clock offsets of warps 1-3 vs warp 0: {cal[1:].tolist()}")
+    for b in range(63):
+        for sl, w in owner.items():
+            if t[g, b, sl]:
+                t[g, b, sl] -= cal[w]
+nb = (H + 31) // 32
+names = ["tri", "build", "bulk0", "bulk1", "bulk2", "bulk3", "rel1", "new0", "new1", "new2", "new3", "end"]
+slots = [1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12]
+for g in range(4):
+    print(f"group {g}: block start-to-start cycles and phase ends (relative to block start)")
+    print("  b  " + " ".join(f"{n:>6s}" for n in names))
+    tot = 0
+    for b in range(nb):
+        r = t[g, b]
+        if r[0] == 0:
+            continue
+        rel = [(int(r[s] - r[0]) if r[s] else -1) for s in slots]
+        tot += rel[-1]
+        print(f" {b:2d}  " + " ".join(f"{x:6d}" for x in rel))
+    print(f"  column total {tot} cycles")
