@@ -173,12 +173,18 @@ __global__ void __launch_bounds__(kRedThreads) reduce_kernel(ReduceArgs a) {
 constexpr int kCW = 4;                 // warps per column
 
 // Diagnostic phase timeline (build with -DSTX_TRACE; scripts/trace_phases.py):
-// CTA 0's column groups record clock64 stamps of their first column's phases.
+// CTA 0's column groups record %globaltimer stamps (ns; one clock for all SM
+// sub-partitions) of their first column's phases.
 #ifdef STX_TRACE
+__device__ __forceinline__ unsigned long long stx_globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 #define STX_STAMP(blk, slot)                                                             \
   do {                                                                                   \
     if (blockIdx.x == 0 && first_item && lane == 0 && (blk) < 64)                        \
-      a.trace[(cslot * 64 + (blk)) * 16 + (slot)] = clock64();                           \
+      a.trace[(cslot * 64 + (blk)) * 16 + (slot)] = stx_globaltimer();                  \
   } while (0)
 #else
 #define STX_STAMP(blk, slot) do { } while (0)

@@ -36,21 +36,12 @@ for _ in range(2):
     assert lib.stixels_compute(h, P(disp), ctypes.c_int64(W * 2), batch, P(out), P(cnt), None) == 0
 torch.cuda.synchronize()
 t = tr.cpu().numpy().reshape(4, 64, 16).astype(np.int64)
-# per-warp clock offsets (warps of a group sit on different SM sub-partitions):
-# calibration stamps right after a common barrier, block slot 63, positions w
-owner = {1: 0, 2: 1, 3: 0, 4: 1, 5: 2, 6: 3, 7: 0, 8: 0, 9: 1, 10: 2, 11: 3, 12: 0}
-for g in range(4):
-    cal = t[g, 63, :4] - t[g, 63, 0]
-    print(f"group {g}: clock offsets of warps 1-3 vs warp 0: {cal[1:].tolist()}")
-    for b in range(63):
-        for sl, w in owner.items():
-            if t[g, b, sl]:
-                t[g, b, sl] -= cal[w]
+t = t * 1.965          # globaltimer ns -> cycles at 1965 MHz
 nb = (H + 31) // 32
 names = ["tri", "build", "bulk0", "bulk1", "bulk2", "bulk3", "rel1", "new0", "new1", "new2", "new3", "end"]
 slots = [1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12]
 for g in range(4):
-    print(f"group {g}: block start-to-start cycles and phase ends (relative to block start)")
+    print(f"group {g}: block start-to-start ~cycles (globaltimer ns x 1.965) and phase ends (relative to block start)")
     print("  b  " + " ".join(f"{n:>6s}" for n in names))
     tot = 0
     for b in range(nb):
