@@ -511,8 +511,14 @@ static int launch_reduce(stixels_handle* h, const void* d_disp, int64_t pitch, i
   r.vec = ((uintptr_t)d_disp % 16 == 0) && (pitch % 16 == 0);
   r.out = d_cols;
   dim3 grid((h->n_cols + h->red_tc - 1) / h->red_tc, (h->H + kRedRows - 1) / kRedRows, batch);
-  if (h->p.reduce_mode == STIXELS_REDUCE_MEDIAN) reduce_kernel<true><<<grid, kRedThreads, h->red_smem, s>>>(r);
-  else reduce_kernel<false><<<grid, kRedThreads, h->red_smem, s>>>(r);
+  const bool med = h->p.reduce_mode == STIXELS_REDUCE_MEDIAN;
+  if (r.bpp == 2) {
+    if (med) reduce_kernel<true, 2><<<grid, kRedThreads, h->red_smem, s>>>(r);
+    else reduce_kernel<false, 2><<<grid, kRedThreads, h->red_smem, s>>>(r);
+  } else {
+    if (med) reduce_kernel<true, 1><<<grid, kRedThreads, h->red_smem, s>>>(r);
+    else reduce_kernel<false, 1><<<grid, kRedThreads, h->red_smem, s>>>(r);
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(h, STIXELS_ERR_CUDA, std::string("reduce_kernel: ") + cudaGetErrorString(e));
   return STIXELS_OK;

@@ -54,9 +54,14 @@ __host__ __device__ inline int red_tile_words(int tc, int s, int bpp) {
   return (((tc * s * bpp + 32 + 15) / 16 * 16) / 4) | 1;   // odd word stride
 }
 
-template <bool MEDIAN>
+template <bool MEDIAN, int BPP>
 __global__ void __launch_bounds__(kRedThreads) reduce_kernel(ReduceArgs a) {
   extern __shared__ uint32_t tile32[];           // [kRedRows][w2] raw input bytes
+  // floor(x / d) for d = 2n <= 2 kMedianMaxS... via a multiply-high by floor(2^32/d)
+  // and one correction step (exact for 32-bit x); the table is per CTA
+  __shared__ uint32_t rcp[2 * kMedianMaxS + 2];
+  for (int i = threadIdx.x; i < 2 * kMedianMaxS + 2; i += kRedThreads)
+    rcp[i] = i < 2 ? 0u : (uint32_t)((1ull << 32) / (unsigned)i);
   const int frame = blockIdx.z;
   const int r0 = blockIdx.y * kRedRows;
   const int c0 = blockIdx.x * a.tc;
@@ -74,17 +79,32 @@ __global__ void __launch_bounds__(kRedThreads) reduce_kernel(ReduceArgs a) {
     const int t = threadIdx.x;
     const int rstep = kRedThreads / nvec;
     const int v = t % nvec;
-    for (int rr = t / nvec; rr < nrows && t < rstep * nvec; rr += rstep) {
-      const uint4 x = __ldg(reinterpret_cast<const uint4*>(base + (int64_t)rr * a.pitch + bs) + v);
-      uint32_t* d = tile32 + rr * a.w2 + 4 * v;
-      d[0] = x.x; d[1] = x.y; d[2] = x.z; d[3] = x.w;
+    const int rb = t / nvec;
+    if (t < rstep * nvec) {
+      // this thread's rows rb, rb + rstep, ...: four 16-byte loads in flight at a time
+      for (int r0i = rb; r0i < nrows; r0i += 4 * rstep) {
+        uint4 x[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int rr = r0i + u * rstep;
+          if (rr < nrows) x[u] = __ldg(reinterpret_cast<const uint4*>(base + (int64_t)rr * a.pitch + bs) + v);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int rr = r0i + u * rstep;
+          if (rr < nrows) {
+            uint32_t* d = tile32 + rr * a.w2 + 4 * v;
+            d[0] = x[u].x; d[1] = x[u].y; d[2] = x[u].z; d[3] = x[u].w;
+          }
+        }
+      }
     }
   } else {
     off = 0;
     for (int i = threadIdx.x; i < nrows * px; i += kRedThreads) {
       const int r = i / px, x = i - r * px;
       const uint8_t* row = base + (int64_t)r * a.pitch + b0;
-      if (a.bpp == 2)
+      if constexpr (BPP == 2)
         reinterpret_cast<uint16_t*>(tile32)[r * 2 * a.w2 + x] = __ldg(reinterpret_cast<const uint16_t*>(row) + x);
       else
         reinterpret_cast<uint8_t*>(tile32)[r * 4 * a.w2 + x] = __ldg(row + x);
@@ -97,11 +117,13 @@ __global__ void __launch_bounds__(kRedThreads) reduce_kernel(ReduceArgs a) {
     const int cl = i / kRedRows, rr = kRedRows - 1 - (i - cl * kRedRows);  // v ascending
     if (rr >= nrows) continue;
     const int e0 = off + cl * a.s;
+    const int rowe = rr * (4 / BPP) * a.w2 + e0;   // element index of the segment start
     auto px_at = [&](int x) -> uint32_t {
-      return a.bpp == 2 ? reinterpret_cast<const uint16_t*>(tile32)[rr * 2 * a.w2 + e0 + x]
-                        : reinterpret_cast<const uint8_t*>(tile32)[rr * 4 * a.w2 + e0 + x];
+      if constexpr (BPP == 2) return reinterpret_cast<const uint16_t*>(tile32)[rowe + x];
+      else return reinterpret_cast<const uint8_t*>(tile32)[rowe + x];
     };
     uint32_t sum = 0, n = 0;
+#pragma unroll 5
     for (int x = 0; x < a.s; ++x) {
       const uint32_t u = px_at(x);
       const bool ok = (u != a.invalid) && (u < lim);
@@ -134,8 +156,13 @@ __global__ void __launch_bounds__(kRedThreads) reduce_kernel(ReduceArgs a) {
       // round half up of 2^R*sum/(2^Q*n) = floor((sum*2^(R+1-Q) + n) / (2n)); 32-bit
       // when it cannot overflow (sum < 2^(31-shift))
       uint32_t q;
-      if (sum < (1u << (31 - shift))) q = ((sum << shift) + n) / (2u * n);
-      else q = (uint32_t)((((uint64_t)sum << shift) + n) / (2ull * n));
+      if (sum < (1u << (31 - shift)) && n <= (uint32_t)kMedianMaxS) {
+        const uint32_t num = (sum << shift) + n, d = 2u * n;
+        q = __umulhi(num, rcp[d]);
+        if (num - q * d >= d) ++q;                   // floor(2^32/d) under-estimates by <= 1
+      } else {
+        q = (uint32_t)((((uint64_t)sum << shift) + n) / (2ull * n));
+      }
       // below D - 1/2 (L#27): the pixel's integer disparity indexes the D x D LUT
       val = (uint16_t)min(q, ((uint32_t)(a.D - 1) << kRBits) + (1u << (kRBits - 1)) - 1u);
     }
