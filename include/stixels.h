@@ -47,6 +47,9 @@ extern "C" {
 /* ---- input formats ------------------------------------------------------- */
 #define STIXELS_U8 0  /* uint8 fixed point, disp_frac_bits fractional bits  */
 #define STIXELS_U16 1 /* uint16 fixed point, disp_frac_bits fractional bits */
+#define STIXELS_F32 2 /* float32 disparity in pixels; invalid if not finite, negative
+                         or >= D (invalid_value and disp_frac_bits unused); a valid
+                         value is converted once to 1/256 px, half up (L#28) */
 
 /* ---- column reduction (a2) ---------------------------------------------- */
 #define STIXELS_REDUCE_MEAN 0   /* mean of the valid pixels of the s-wide segment */
@@ -96,7 +99,7 @@ typedef struct stixels_params {
   int32_t stixel_width;  /* s >= 1                                          */
   int32_t max_disparity; /* D = d_range, 2 <= D <= 256                     */
   /* --- input encoding (a1) ----------------------------------------------- */
-  int32_t disp_format;   /* STIXELS_U8 or STIXELS_U16                             */
+  int32_t disp_format;   /* STIXELS_U8, STIXELS_U16 or STIXELS_F32                */
   int32_t disp_frac_bits;/* Q: fractional bits of the input, 0..8                 */
   uint32_t invalid_value;/* sentinel of an invalid pixel; values decoding to >= D
                             are invalid too (L#23)                                */

@@ -124,6 +124,26 @@ long long orc_ground_R(const orc_model* m, int v) {
  * clamped to below D - 1/2 (L#27): the pair LUT of P:175 is D x D, so a
  * pixel's integer disparity round_half_up(d') must lie in [0, D).
  * ------------------------------------------------------------------------ */
+/* One input pixel (a1).  u8/u16: the raw fixed-point value (Q_bits fractional
+ * bits), invalid if it equals `invalid` or decodes to >= D.  f32 (bytes_per_px 4,
+ * DESIGN.md L#28): a disparity in pixels, invalid if not finite, negative or
+ * >= D; a valid value is converted once to the 1/2^8 grid, half up:
+ * u = floor(256 d + 1/2) (the caller then uses Q_bits = 8).  Returns validity. */
+static int pixel_value(const void* img, int bytes_per_px, long long idx, unsigned int invalid,
+                       int D, int Q_bits, unsigned int* u) {
+  if (bytes_per_px == 4) {
+    double d = (double)((const float*)img)[idx];
+    if (!isfinite(d) || d < 0.0 || d >= (double)D) return 0;
+    *u = (unsigned int)floor(d * 256.0 + 0.5);
+    return 1;
+  }
+  unsigned int x = bytes_per_px == 1 ? ((const uint8_t*)img)[idx] : ((const uint16_t*)img)[idx];
+  if (x == invalid) return 0;
+  if ((long long)x >= ((long long)D << Q_bits)) return 0; /* d >= D: invalid */
+  *u = x;
+  return 1;
+}
+
 static int clamp_reduced(long long x, int D, int R_bits) {
   long long mx = ((long long)(D - 1) << R_bits) + (1LL << (R_bits - 1)) - 1;
   return (int)(x < mx ? x : mx);
@@ -131,17 +151,14 @@ static int clamp_reduced(long long x, int D, int R_bits) {
 void orc_reduce(const void* img, int bytes_per_px, int W, int H, long long pitch_px, int s,
                 int Q_bits, unsigned int invalid, int D, int R_bits, int* out) {
   int n_cols = W / s;
+  if (bytes_per_px == 4) Q_bits = 8;   /* f32: values converted to the 1/256 grid */
   for (int c = 0; c < n_cols; ++c) {
     for (int r = 0; r < H; ++r) {
       long long sum = 0, n = 0;
       for (int x = c * s; x < c * s + s; ++x) {
         unsigned int u;
-        if (bytes_per_px == 1)
-          u = ((const uint8_t*)img)[(long long)r * pitch_px + x];
-        else
-          u = ((const uint16_t*)img)[(long long)r * pitch_px + x];
-        if (u == invalid) continue;
-        if ((long long)u >= ((long long)D << Q_bits)) continue; /* d >= D: invalid */
+        if (!pixel_value(img, bytes_per_px, (long long)r * pitch_px + x, invalid, D, Q_bits, &u))
+          continue;
         sum += u;
         n += 1;
       }
@@ -176,18 +193,15 @@ static int cmp_uint(const void* a, const void* b) {
 void orc_reduce_median(const void* img, int bytes_per_px, int W, int H, long long pitch_px,
                        int s, int Q_bits, unsigned int invalid, int D, int R_bits, int* out) {
   int n_cols = W / s;
+  if (bytes_per_px == 4) Q_bits = 8;   /* f32: values converted to the 1/256 grid */
   unsigned int* vals = (unsigned int*)malloc(sizeof(unsigned int) * (size_t)(s > 0 ? s : 1));
   for (int c = 0; c < n_cols; ++c) {
     for (int r = 0; r < H; ++r) {
       int n = 0;
       for (int x = c * s; x < c * s + s; ++x) {
         unsigned int u;
-        if (bytes_per_px == 1)
-          u = ((const uint8_t*)img)[(long long)r * pitch_px + x];
-        else
-          u = ((const uint16_t*)img)[(long long)r * pitch_px + x];
-        if (u == invalid) continue;
-        if ((long long)u >= ((long long)D << Q_bits)) continue; /* d >= D: invalid */
+        if (!pixel_value(img, bytes_per_px, (long long)r * pitch_px + x, invalid, D, Q_bits, &u))
+          continue;
         vals[n++] = u;
       }
       int v = H - 1 - r;

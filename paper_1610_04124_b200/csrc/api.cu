@@ -56,6 +56,8 @@ struct stixels_handle {
 
 static thread_local std::string g_create_err;
 
+static int bytes_per_px(int fmt) { return fmt == STIXELS_F32 ? 4 : fmt == STIXELS_U16 ? 2 : 1; }
+
 static int fail(stixels_handle* h, int code, const std::string& msg) {
   if (h) {
     h->err = msg;
@@ -163,7 +165,9 @@ int validate(const stixels_params* p, int W, int H, int max_batch, std::string& 
   if (p->ord_margin < 0 || p->grav_margin < 0 || p->ord_margin > 255 || p->grav_margin > 255) {
     msg = "margins must be in [0, 255]"; return STIXELS_ERR_PARAM;
   }
-  if (p->disp_format != STIXELS_U8 && p->disp_format != STIXELS_U16) { msg = "disp_format must be U8 or U16"; return STIXELS_ERR_PARAM; }
+  if (p->disp_format != STIXELS_U8 && p->disp_format != STIXELS_U16 && p->disp_format != STIXELS_F32) {
+    msg = "disp_format must be U8, U16 or F32"; return STIXELS_ERR_PARAM;
+  }
   if (p->disp_frac_bits < 0 || p->disp_frac_bits > 8) { msg = "disp_frac_bits must be in [0, 8]"; return STIXELS_ERR_PARAM; }
   if (p->reduce_mode != STIXELS_REDUCE_MEAN && p->reduce_mode != STIXELS_REDUCE_MEDIAN) {
     msg = "reduce_mode must be STIXELS_REDUCE_MEAN (P:195) or STIXELS_REDUCE_MEDIAN"; return STIXELS_ERR_UNSUPPORTED;
@@ -445,8 +449,9 @@ int stixels_create(const stixels_params* params, int width, int height, int max_
   if (e != cudaSuccess || per_sm < 1) return bail(STIXELS_ERR_UNSUPPORTED, "dp_kernel does not fit on an SM");
   h->grid = h->sms * per_sm;
   // reduction tile
-  h->red_tc = std::max(1, std::min(h->n_cols, 512 / params->stixel_width));
-  h->red_w2 = red_tile_words(h->red_tc, params->stixel_width, params->disp_format == STIXELS_U16 ? 2 : 1);
+  const int in_bpp = bytes_per_px(params->disp_format);
+  h->red_tc = std::max(1, std::min(h->n_cols, (in_bpp == 4 ? 256 : 512) / params->stixel_width));
+  h->red_w2 = red_tile_words(h->red_tc, params->stixel_width, in_bpp);
   h->red_smem = kRedRows * h->red_w2 * 4;
 
   auto alloc = [&](void** ptr, size_t n) { return cudaMalloc(ptr, n); };
@@ -504,15 +509,19 @@ static int launch_reduce(stixels_handle* h, const void* d_disp, int64_t pitch, i
                          uint16_t* d_cols, cudaStream_t s) {
   ReduceArgs r;
   r.disp = (const uint8_t*)d_disp; r.pitch = pitch; r.W = h->W; r.H = h->H; r.n_cols = h->n_cols;
-  r.s = h->p.stixel_width; r.tc = h->red_tc; r.q_bits = h->p.disp_frac_bits; r.D = h->p.max_disparity;
-  r.bpp = h->p.disp_format == STIXELS_U16 ? 2 : 1;
+  r.bpp = bytes_per_px(h->p.disp_format);
+  r.s = h->p.stixel_width; r.tc = h->red_tc; r.D = h->p.max_disparity;
+  r.q_bits = r.bpp == 4 ? 8 : h->p.disp_frac_bits;   // f32: converted to the 1/256 grid (L#28)
   r.invalid = h->p.invalid_value;
   r.w2 = h->red_w2;
   r.vec = ((uintptr_t)d_disp % 16 == 0) && (pitch % 16 == 0);
   r.out = d_cols;
   dim3 grid((h->n_cols + h->red_tc - 1) / h->red_tc, (h->H + kRedRows - 1) / kRedRows, batch);
   const bool med = h->p.reduce_mode == STIXELS_REDUCE_MEDIAN;
-  if (r.bpp == 2) {
+  if (r.bpp == 4) {
+    if (med) reduce_kernel<true, 4><<<grid, kRedThreads, h->red_smem, s>>>(r);
+    else reduce_kernel<false, 4><<<grid, kRedThreads, h->red_smem, s>>>(r);
+  } else if (r.bpp == 2) {
     if (med) reduce_kernel<true, 2><<<grid, kRedThreads, h->red_smem, s>>>(r);
     else reduce_kernel<false, 2><<<grid, kRedThreads, h->red_smem, s>>>(r);
   } else {
@@ -548,7 +557,7 @@ static int launch_dp(stixels_handle* h, const uint16_t* d_cols, int batch, stixe
 static int check_disp_args(stixels_handle* h, const void* d, int64_t pitch, int batch) {
   if (!h) return STIXELS_ERR_ARG;
   if (h->sticky) return h->sticky;
-  int bpp = h->p.disp_format == STIXELS_U16 ? 2 : 1;
+  int bpp = bytes_per_px(h->p.disp_format);
   if (!d || batch < 1 || batch > h->max_batch || pitch < (int64_t)h->W * bpp || (pitch % bpp))
     return fail(h, STIXELS_ERR_ARG, "bad input pointer, batch or row pitch");
   return STIXELS_OK;
@@ -590,7 +599,7 @@ int stixels_compute_host(stixels_handle* h, const void* h_disp, int64_t pitch, i
                          stixel_t* h_out, int32_t* h_count, float* h_cost) {
   if (!h) return STIXELS_ERR_ARG;
   if (h->sticky) return h->sticky;
-  int bpp = h->p.disp_format == STIXELS_U16 ? 2 : 1;
+  int bpp = bytes_per_px(h->p.disp_format);
   if (!h_disp || !h_out || !h_count || batch < 1 || pitch < (int64_t)h->W * bpp)
     return fail(h, STIXELS_ERR_ARG, "bad host pointer, batch or pitch");
   cudaSetDevice(h->device);

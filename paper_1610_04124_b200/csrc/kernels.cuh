@@ -104,7 +104,9 @@ __global__ void __launch_bounds__(kRedThreads) reduce_kernel(ReduceArgs a) {
     for (int i = threadIdx.x; i < nrows * px; i += kRedThreads) {
       const int r = i / px, x = i - r * px;
       const uint8_t* row = base + (int64_t)r * a.pitch + b0;
-      if constexpr (BPP == 2)
+      if constexpr (BPP == 4)
+        tile32[r * a.w2 + x] = __ldg(reinterpret_cast<const uint32_t*>(row) + x);
+      else if constexpr (BPP == 2)
         reinterpret_cast<uint16_t*>(tile32)[r * 2 * a.w2 + x] = __ldg(reinterpret_cast<const uint16_t*>(row) + x);
       else
         reinterpret_cast<uint8_t*>(tile32)[r * 4 * a.w2 + x] = __ldg(row + x);
@@ -118,15 +120,26 @@ __global__ void __launch_bounds__(kRedThreads) reduce_kernel(ReduceArgs a) {
     if (rr >= nrows) continue;
     const int e0 = off + cl * a.s;
     const int rowe = rr * (4 / BPP) * a.w2 + e0;   // element index of the segment start
-    auto px_at = [&](int x) -> uint32_t {
-      if constexpr (BPP == 2) return reinterpret_cast<const uint16_t*>(tile32)[rowe + x];
-      else return reinterpret_cast<const uint8_t*>(tile32)[rowe + x];
+    // a pixel: its value in input units (f32: converted once to the 1/256 grid,
+    // half up, L#28) and validity
+    const float Df = (float)a.D;
+    auto px_ok = [&](int x, uint32_t& u) -> bool {
+      if constexpr (BPP == 4) {
+        const float d = __uint_as_float(tile32[rowe + x]);
+        const bool ok = d >= 0.f && d < Df;           // false for NaN and +-inf too
+        u = ok ? (uint32_t)__float2int_rd(d * 256.f + 0.5f) : 0u;   // exact: d * 256 < 2^16
+        return ok;
+      } else {
+        u = BPP == 2 ? reinterpret_cast<const uint16_t*>(tile32)[rowe + x]
+                     : reinterpret_cast<const uint8_t*>(tile32)[rowe + x];
+        return (u != a.invalid) && (u < lim);
+      }
     };
     uint32_t sum = 0, n = 0;
 #pragma unroll 5
     for (int x = 0; x < a.s; ++x) {
-      const uint32_t u = px_at(x);
-      const bool ok = (u != a.invalid) && (u < lim);
+      uint32_t u;
+      const bool ok = px_ok(x, u);
       sum += ok ? u : 0u;
       n += ok ? 1u : 0u;
     }
@@ -136,12 +149,12 @@ __global__ void __launch_bounds__(kRedThreads) reduce_kernel(ReduceArgs a) {
       const uint32_t k1 = (n - 1) >> 1, k2 = n >> 1;
       uint32_t va = 0, vb = 0;
       for (int x = 0; x < a.s; ++x) {
-        const uint32_t u = px_at(x);
-        if (u == a.invalid || u >= lim) continue;
+        uint32_t u;
+        if (!px_ok(x, u)) continue;
         uint32_t less = 0, leq = 0;
         for (int y = 0; y < a.s; ++y) {
-          const uint32_t t = px_at(y);
-          const bool ok = (t != a.invalid) && (t < lim);
+          uint32_t t;
+          const bool ok = px_ok(y, t);
           less += (ok && t < u) ? 1u : 0u;
           leq += (ok && t <= u) ? 1u : 0u;
         }

@@ -15,7 +15,7 @@ import numpy as np
 from .build import LIB
 
 GROUND, OBJECT, SKY = 0, 1, 2
-U8, U16 = 0, 1
+U8, U16, F32 = 0, 1, 2
 REDUCE_MEAN, REDUCE_MEDIAN = 0, 1
 
 OK, ERR_ARG, ERR_PARAM, ERR_UNSUPPORTED, ERR_CUDA, ERR_CAPACITY = 0, -1, -2, -3, -4, -5

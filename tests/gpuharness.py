@@ -8,7 +8,7 @@ from tests import modelparams as mp
 
 
 def run_gpu(p: dict, frames: np.ndarray, max_batch: int | None = None, host: bool = False):
-    """frames: [B][H][W] uint16/uint8 -> (lists per frame per column, costs [B][n_cols],
+    """frames: [B][H][W] uint16/uint8/float32 -> (lists per frame per column, costs [B][n_cols],
     counts [B][n_cols], handle)."""
     import torch
     from paper_1610_04124_b200 import stixels as S
@@ -16,6 +16,8 @@ def run_gpu(p: dict, frames: np.ndarray, max_batch: int | None = None, host: boo
     params = S.params_from_dict(p, H)
     if frames.dtype == np.uint8:
         params.disp_format = S.U8
+    elif frames.dtype == np.float32:
+        params.disp_format = S.F32
     hd = S.Handle(params, W, H, max_batch or B)
     if host:
         out = np.zeros((B, hd.n_cols, hd.cap, 12), np.uint8)

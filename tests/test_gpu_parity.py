@@ -147,6 +147,40 @@ def test_reduce_vector_path_bit_exact(W, s, fmt):
         hd.destroy()
 
 
+@pytest.mark.parametrize("W,s", [(1024, 5), (1027, 3), (64, 64)])
+def test_reduce_f32_bit_exact(W, s):
+    """f32 input (L#28): NaN / inf / negative / >= D invalid, half-up conversion to
+    1/256, mean and median; vector (W = 1024) and scalar (odd pitch) load paths."""
+    import torch
+    from oracle import oracle as orc
+    from paper_1610_04124_b200 import stixels as S
+    H, D = 50, 64
+    rng = np.random.default_rng(W + s)
+    f = rng.uniform(-2.0, D + 2.0, size=(2, H, W)).astype(np.float32)
+    f[rng.random(f.shape) < 0.05] = np.nan
+    f[rng.random(f.shape) < 0.02] = np.inf
+    f[:, :, :7] = np.round(f[:, :, :7] * 256) / 256 + np.float32(1 / 512)   # exact half-way values
+    for mode in (0, 1):
+        p = mp.make(max_disparity=D, stixel_width=s, reduce_mode=mode, disp_format=S.F32)
+        hd = S.Handle(S.params_from_dict(p, H), W, H, 2)
+        cols = torch.empty((2, hd.n_cols, H), dtype=torch.int16, device="cuda")
+        hd.reduce(torch.from_numpy(f).cuda(), cols)
+        hd.sync()
+        got = cols.cpu().numpy().view(np.uint16).astype(np.int32)
+        got[got == 0xFFFF] = -1
+        for b in range(2):
+            assert (got[b] == orc.reduce(f[b], s, 0, 0, D, mode=mode)).all(), (mode, b)
+        hd.destroy()
+
+
+def test_f32_input_end_to_end_exact():
+    frames = _frames_c2(1, seed0=2900)
+    f = np.where(frames == 0xFFFF, np.nan, frames.astype(np.float64) / 16).astype(np.float32)
+    from paper_1610_04124_b200 import stixels as S
+    p = mp.make(disp_format=S.F32)
+    _assert_exact(p, f)
+
+
 def test_c1_scene_exact():
     sc = synth.c1_scene()
     frames = np.stack([synth.render(sc, 1, noise=False), synth.render(sc, 2)])

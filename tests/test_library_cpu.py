@@ -64,7 +64,7 @@ def _create(p, W=1024, H=440, B_=1):
     ("p_out", 0.0, S.ERR_PARAM), ("p_out", 1.0, S.ERR_PARAM), ("max_disparity", 1, S.ERR_PARAM),
     ("max_disparity", 300, S.ERR_UNSUPPORTED), ("stixel_width", 0, S.ERR_PARAM),
     ("a_norm", 0.0, S.ERR_PARAM), ("p_ord", 1.5, S.ERR_PARAM), ("ord_margin", -1, S.ERR_PARAM),
-    ("disp_frac_bits", 9, S.ERR_PARAM), ("reduce_mode", 2, S.ERR_UNSUPPORTED),
+    ("disp_frac_bits", 9, S.ERR_PARAM), ("disp_format", 3, S.ERR_PARAM), ("reduce_mode", 2, S.ERR_UNSUPPORTED),
     ("cost_frac_bits", 30, S.ERR_PARAM), ("horizon_row", float("inf"), S.ERR_PARAM),
 ])
 def test_param_validation(field, value, code):
