@@ -152,14 +152,13 @@ def measured_peaks():
         return {}
 
 
-def ncu_traffic_per_frame():
-    """DRAM bytes per frame of the DP kernel from the committed ncu --set full
-    capture (profiles/), or None."""
+def ncu_profile():
+    """The committed ncu --set full capture of the DP kernel (profiles/): DRAM bytes
+    per frame and measured pipe utilisations, or {}."""
     try:
-        d = json.load(open(os.path.join(ROOT, "profiles", "dp_kernel_ncu.json")))
-        return d["dram_bytes_per_frame"]
+        return json.load(open(os.path.join(ROOT, "profiles", "dp_kernel_ncu.json")))
     except Exception:
-        return None
+        return {}
 
 
 def cpu_baseline(p, pool, frames_req=0):
@@ -438,14 +437,24 @@ def main():
     dp_ms = statistics.mean(dp)
     cells = cells_per_frame() * B
     achieved = cells * ALG_OPS_PER_CELL / (dp_ms / 1000.0) / 1e12
-    tpf = ncu_traffic_per_frame()
+    prof = ncu_profile()
+    tpf = prof.get("dram_bytes_per_frame")
     roofline = {"bound": "alu", "achieved": achieved, "peak": peak_tops, "unit": "Tops/s",
                 "frac": achieved / peak_tops,
                 "traffic": (tpf * B) if tpf is not None else None,
                 "kernel": "dp_kernel", "ops_per_cell": ALG_OPS_PER_CELL,
                 "cells_per_launch": cells,
                 "peak_note": f"{n_sm} SMs x 128 lanes x {sm_max:.0f} MHz (issue peak, "
-                             "B200_PROFILING/B300_MICROARCH unit counts; DESIGN.md 6)"}
+                             "B200_PROFILING/B300_MICROARCH unit counts; DESIGN.md 5b)",
+                "ncu_pipe_util": prof.get("pipe_util")}
+    # K1 (a1-a2) against HBM: algorithmic bytes = input read + reduced columns written
+    red_ms = statistics.mean(red)
+    red_bytes = B * (W_IMG * H_IMG * 2 + (W_IMG // S_W) * H_IMG * 2)
+    hbm_peak = peaks.get("hbm_gbs", 6555.2)
+    k1_roofline = {"bound": "hbm", "kernel": "reduce_kernel", "unit": "GB/s",
+                   "achieved": red_bytes / (red_ms / 1000.0) / 1e9, "peak": hbm_peak,
+                   "frac": red_bytes / (red_ms / 1000.0) / 1e9 / hbm_peak,
+                   "bytes_per_launch": red_bytes}
 
     # end-to-end through the C ABI with host buffers (pinned), copies included
     e2e = None
@@ -497,7 +506,7 @@ def main():
             "cells_per_s": cells_per_frame() * frames_total / (max_ms / 1000.0),
             "stage_ms": {"reduce": statistics.mean(red), "dp": dp_ms},
             "stage_share": {"reduce": sum(red) / total_ms, "dp": sum(dp) / total_ms},
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roofline, "k1_roofline": k1_roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": 2 * args.steps, "clocks": clocks, "parity": parity,
             "fps_per_watt": (value / world / clocks["power_w"]) if clocks.get("power_w") else None,
         }

@@ -518,15 +518,15 @@ static int launch_reduce(stixels_handle* h, const void* d_disp, int64_t pitch, i
   r.out = d_cols;
   dim3 grid((h->n_cols + h->red_tc - 1) / h->red_tc, (h->H + kRedRows - 1) / kRedRows, batch);
   const bool med = h->p.reduce_mode == STIXELS_REDUCE_MEDIAN;
+  const bool s5 = r.s == 5;                          // the headline width, compile-time
+  auto go = [&](auto kern) { kern<<<grid, kRedThreads, h->red_smem, s>>>(r); };
   if (r.bpp == 4) {
-    if (med) reduce_kernel<true, 4><<<grid, kRedThreads, h->red_smem, s>>>(r);
-    else reduce_kernel<false, 4><<<grid, kRedThreads, h->red_smem, s>>>(r);
+    if (med) go(reduce_kernel<true, 4, 0>); else go(reduce_kernel<false, 4, 0>);
   } else if (r.bpp == 2) {
-    if (med) reduce_kernel<true, 2><<<grid, kRedThreads, h->red_smem, s>>>(r);
-    else reduce_kernel<false, 2><<<grid, kRedThreads, h->red_smem, s>>>(r);
+    if (med) { if (s5) go(reduce_kernel<true, 2, 5>); else go(reduce_kernel<true, 2, 0>); }
+    else { if (s5) go(reduce_kernel<false, 2, 5>); else go(reduce_kernel<false, 2, 0>); }
   } else {
-    if (med) reduce_kernel<true, 1><<<grid, kRedThreads, h->red_smem, s>>>(r);
-    else reduce_kernel<false, 1><<<grid, kRedThreads, h->red_smem, s>>>(r);
+    if (med) go(reduce_kernel<true, 1, 0>); else go(reduce_kernel<false, 1, 0>);
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(h, STIXELS_ERR_CUDA, std::string("reduce_kernel: ") + cudaGetErrorString(e));

@@ -54,8 +54,10 @@ __host__ __device__ inline int red_tile_words(int tc, int s, int bpp) {
   return (((tc * s * bpp + 32 + 15) / 16 * 16) / 4) | 1;   // odd word stride
 }
 
-template <bool MEDIAN, int BPP>
+// SW > 0: the stixel width as a compile-time constant (the headline s = 5), 0: a.s
+template <bool MEDIAN, int BPP, int SW>
 __global__ void __launch_bounds__(kRedThreads) reduce_kernel(ReduceArgs a) {
+  const int sw = SW > 0 ? SW : a.s;
   extern __shared__ uint32_t tile32[];           // [kRedRows][w2] raw input bytes
   // floor(x / d) for d = 2n <= 2 kMedianMaxS... via a multiply-high by floor(2^32/d)
   // and one correction step (exact for 32-bit x); the table is per CTA
@@ -66,10 +68,10 @@ __global__ void __launch_bounds__(kRedThreads) reduce_kernel(ReduceArgs a) {
   const int r0 = blockIdx.y * kRedRows;
   const int c0 = blockIdx.x * a.tc;
   const int ncl = min(a.tc, a.n_cols - c0);
-  const int px = ncl * a.s;
+  const int px = ncl * sw;
   const int nrows = min(kRedRows, a.H - r0);
   const uint8_t* base = a.disp + (int64_t)frame * a.H * a.pitch + (int64_t)r0 * a.pitch;
-  const int b0 = c0 * a.s * a.bpp;                 // first byte of the tile in a row
+  const int b0 = c0 * sw * BPP;                    // first byte of the tile in a row
   int off;                                         // element offset of pixel c0*s in the tile
   if (a.vec) {
     const int bs = b0 & ~15;
@@ -118,7 +120,7 @@ __global__ void __launch_bounds__(kRedThreads) reduce_kernel(ReduceArgs a) {
   for (int i = threadIdx.x; i < ncl * kRedRows; i += kRedThreads) {
     const int cl = i / kRedRows, rr = kRedRows - 1 - (i - cl * kRedRows);  // v ascending
     if (rr >= nrows) continue;
-    const int e0 = off + cl * a.s;
+    const int e0 = off + cl * sw;
     const int rowe = rr * (4 / BPP) * a.w2 + e0;   // element index of the segment start
     // a pixel: its value in input units (f32: converted once to the 1/256 grid,
     // half up, L#28) and validity
@@ -137,7 +139,7 @@ __global__ void __launch_bounds__(kRedThreads) reduce_kernel(ReduceArgs a) {
     };
     uint32_t sum = 0, n = 0;
 #pragma unroll 5
-    for (int x = 0; x < a.s; ++x) {
+    for (int x = 0; x < sw; ++x) {
       uint32_t u;
       const bool ok = px_ok(x, u);
       sum += ok ? u : 0u;
@@ -148,11 +150,11 @@ __global__ void __launch_bounds__(kRedThreads) reduce_kernel(ReduceArgs a) {
       // by rank counting (s <= 64, no sort), averaged with the mean's rounding
       const uint32_t k1 = (n - 1) >> 1, k2 = n >> 1;
       uint32_t va = 0, vb = 0;
-      for (int x = 0; x < a.s; ++x) {
+      for (int x = 0; x < sw; ++x) {
         uint32_t u;
         if (!px_ok(x, u)) continue;
         uint32_t less = 0, leq = 0;
-        for (int y = 0; y < a.s; ++y) {
+        for (int y = 0; y < sw; ++y) {
           uint32_t t;
           const bool ok = px_ok(y, t);
           less += (ok && t < u) ? 1u : 0u;
