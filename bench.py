@@ -461,7 +461,7 @@ def main():
     if not args.no_e2e:
         eb = min(args.e2e_batch, B)
         p2 = dict(p, max_stixels=128)
-        hd2 = S.Handle(S.params_from_dict(p2, H_IMG), W_IMG, H_IMG, min(eb, 64), device=local,
+        hd2 = S.Handle(S.params_from_dict(p2, H_IMG), W_IMG, H_IMG, min(eb, 32), device=local,
                        stream=stream)
         hin = torch.empty((eb, H_IMG, W_IMG), dtype=torch.int16).pin_memory()
         hin.copy_(torch.from_numpy(pool[idx[:eb]].view(np.int16)))
@@ -484,7 +484,7 @@ def main():
                "h2d_bytes_per_step": eb * H_IMG * pitch,
                "d2h_bytes_per_step": eb * hd2.n_cols * (hd2.cap * 12 + 8),
                "frames_per_step": eb, "max_stixels": 128,
-               "note": "stixels_compute_host: pinned host buffers, 64-frame chunks on 2 "
+               "note": "stixels_compute_host: pinned host buffers, 32-frame chunks on 2 "
                        "streams, synchronous call; wall clock max over ranks"}
         hd2.destroy()
 

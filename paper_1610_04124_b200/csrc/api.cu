@@ -603,7 +603,7 @@ int stixels_compute_host(stixels_handle* h, const void* h_disp, int64_t pitch, i
   if (!h_disp || !h_out || !h_count || batch < 1 || pitch < (int64_t)h->W * bpp)
     return fail(h, STIXELS_ERR_ARG, "bad host pointer, batch or pitch");
   cudaSetDevice(h->device);
-  const int chunk = std::min(h->max_batch, 64);
+  const int chunk = std::min(h->max_batch, 32);   // frames per H2D / compute / D2H stage
   const size_t in_b = (size_t)h->H * pitch;
   if (h->h_chunk != chunk || h->h_pitch != pitch) {
     for (int i = 0; i < 2; ++i) {
