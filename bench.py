@@ -488,6 +488,29 @@ def main():
                        "streams, synchronous call; wall clock max over ranks"}
         hd2.destroy()
 
+    # BASELINE configs[1]: ONE frame per call (latency; the GPU is mostly idle: 204
+    # columns for 592 column slots), frames back to back, inputs resident
+    single = None
+    if rank == 0:
+        hd1 = S.Handle(params, W_IMG, H_IMG, 1, device=local, stream=stream)
+        o1, c1, k1 = hd1.alloc_outputs(1)
+        with torch.cuda.stream(stream):
+            for i in range(3):
+                hd1.compute(disp[i:i + 1], o1, c1, k1)
+        torch.cuda.synchronize()
+        n1 = 50
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            s0.record(stream)
+            for i in range(n1):
+                hd1.compute(disp[i:i + 1], o1, c1, k1)
+            s1.record(stream)
+        torch.cuda.synchronize()
+        lat_ms = s0.elapsed_time(s1) / n1
+        single = {"workload": "configs[1]: single 1024x440 frame per call (w=5, D=128)",
+                  "latency_us": 1000.0 * lat_ms, "fps": 1000.0 / lat_ms, "calls": n1}
+        hd1.destroy()
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline(p, pool, args.cpu_frames)
@@ -507,6 +530,7 @@ def main():
             "stage_ms": {"reduce": statistics.mean(red), "dp": dp_ms},
             "stage_share": {"reduce": sum(red) / total_ms, "dp": sum(dp) / total_ms},
             "roofline": roofline, "k1_roofline": k1_roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "single_frame": single,
             "gpu_launches": 2 * args.steps, "clocks": clocks, "parity": parity,
             "fps_per_watt": (value / world / clocks["power_w"]) if clocks.get("power_w") else None,
         }

@@ -538,16 +538,22 @@ static int launch_dp(stixels_handle* h, const uint16_t* d_cols, int batch, stixe
   DPArgs A = h->args;
   A.cols = d_cols; A.out = d_out; A.count = d_count; A.col_cost = d_cost;
   A.items = batch * h->n_cols;
-  int grid = std::min(h->grid, (A.items + h->cols_per_cta - 1) / h->cols_per_cta);
-  const int threads = h->cols_per_cta * kCW * 32;
+  // Column groups per CTA: the full count when the batch fills the GPU; fewer when
+  // it does not (e.g. one frame: 204 columns for 148 SMs), so the columns spread
+  // over more SMs instead of sharing a few (latency, BASELINE configs[1]).
+  const int C = std::max(1, std::min(h->cols_per_cta, (A.items + h->sms - 1) / h->sms));
+  A.cols_per_cta = C;
+  const int smem = A.shared_bytes + C * A.col_bytes;
+  int grid = std::min(h->grid, (A.items + C - 1) / C);
+  const int threads = C * kCW * 32;
   if (h->dp_slots == 128) {
-    if (h->pair2d) dp_kernel<128, true, true><<<grid, threads, h->smem, s>>>(A);
-    else if (h->sparse) dp_kernel<128, true, false><<<grid, threads, h->smem, s>>>(A);
-    else dp_kernel<128, false, false><<<grid, threads, h->smem, s>>>(A);
+    if (h->pair2d) dp_kernel<128, true, true><<<grid, threads, smem, s>>>(A);
+    else if (h->sparse) dp_kernel<128, true, false><<<grid, threads, smem, s>>>(A);
+    else dp_kernel<128, false, false><<<grid, threads, smem, s>>>(A);
   } else {
-    if (h->pair2d) dp_kernel<256, true, true><<<grid, threads, h->smem, s>>>(A);
-    else if (h->sparse) dp_kernel<256, true, false><<<grid, threads, h->smem, s>>>(A);
-    else dp_kernel<256, false, false><<<grid, threads, h->smem, s>>>(A);
+    if (h->pair2d) dp_kernel<256, true, true><<<grid, threads, smem, s>>>(A);
+    else if (h->sparse) dp_kernel<256, true, false><<<grid, threads, smem, s>>>(A);
+    else dp_kernel<256, false, false><<<grid, threads, smem, s>>>(A);
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(h, STIXELS_ERR_CUDA, std::string("dp_kernel: ") + cudaGetErrorString(e));
