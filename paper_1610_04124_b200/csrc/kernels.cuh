@@ -911,6 +911,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
         float rB = __shfl_sync(0xffffffffu, best, 1);
         int rF = __shfl_sync(0xffffffffu, argf, 1);
         int off = 0;                                    // tri_off(jp)
+        STX_STAMP(b, 13);                 // serial: merge + recovery + chain setup done
         for (int jp = 0; jp < jn; ++jp) {
           const int j = K0 + jp + 1;                    // bottom j; target j finalised
           const float4 q = cs.pgps[jp + 1];
@@ -950,6 +951,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
           prevF = Fj;
           off += 31 - jp;
         }
+        STX_STAMP(b, 14);                 // serial: triangle chain done
         // ---- ground / sky argmins and values of the block's rows, as warp scans ----
         // lane l = row j = K0 + l = target k: candidates at bottom j use C[j-1]
         const float up_best = __shfl_up_sync(0xffffffffu, best, 1);     // all lanes shuffle
@@ -989,6 +991,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
         if (K0 + 31 >= h - 1) {
           lastO = cCO; lastG = cCG; lastS = __shfl_sync(0xffffffffu, CSk, L);
         }
+        STX_STAMP(b, 15);                 // serial: scans + carries done
         // every lane now holds the final values of its target row k: write the
         // record of row k+1 (consumed by later rectangles; predecessor terms
         // shifted by -cap*(k+1)) and the index table

@@ -38,8 +38,9 @@ torch.cuda.synchronize()
 t = tr.cpu().numpy().reshape(4, 64, 16).astype(np.int64)
 t = t * 1.965          # globaltimer ns -> cycles at 1965 MHz
 nb = (H + 31) // 32
-names = ["tri", "build", "bulk0", "bulk1", "bulk2", "bulk3", "rel1", "new0", "new1", "new2", "new3", "end"]
-slots = [1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12]
+names = ["setup", "chain", "scans", "tri", "build", "bulk0", "bulk1", "bulk2", "bulk3", "rel1", "new0",
+         "new1", "new2", "new3", "end"]
+slots = [13, 14, 15, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12]
 for g in range(4):
     print(f"group {g}: block start-to-start ~cycles (globaltimer ns x 1.965) and phase ends (relative to block start)")
     print("  b  " + " ".join(f"{n:>6s}" for n in names))
