@@ -1,7 +1,7 @@
 #!/usr/bin/env python3
 """Small end-to-end run of the CUDA path for compute-sanitizer (memcheck /
-racecheck / synccheck): a few columns of C1/C2-like frames in exact and
-continuous mode, mean and median reductions, the f2 tables, u8 input, and a
+racecheck / synccheck): a few columns of C1/C2-like frames in exact mode,
+mean and median reductions, the f2 tables, D = 256, and a
 dense-ring (wide band) model; each result checked against the oracle."""
 import os
 import sys
