@@ -191,24 +191,25 @@ __global__ void __launch_bounds__(kRedThreads) reduce_kernel(ReduceArgs a) {
 // K3: DP kernel (prefix sums + object-LUT rows + Eq. 5-6 DP + backtracking).
 //
 // Work unit: one column, handled by a "column group" of kCW = 4 warps with its
-// own named barrier.  Lanes own targets k = K0 + lane of a 32-row block b
-// (K0 = 32 b).  The object LUT LUT_object[f][v] (D x (h+1)) is never
-// materialised; per block, the 32 target rows priv_b[i][f] = LUT[f][K0+i+1]
-// live in shared memory (double-buffered), and the bottom row LUT[.][j] is
-// carried incrementally in a per-warp ring seeded from an anchor row
-// (row_{j+1} = row_j + Pair[.][d_j]).
+// own named barriers (up to 4 groups per CTA, one CTA per SM).  Lanes own targets
+// k = K0 + lane of a 32-row block b (K0 = 32 b).  The object LUT LUT_object[f][v]
+// (D x (h+1)) is never materialised: per block, the 32 target rows
+// priv[i][f] = W[f][K0+i+1] (W = LUT - cap * v, see below) live in shared memory,
+// and the bottom row W[.][j] is carried incrementally in per-warp buffers seeded
+// from an anchor row (W_{j+1} = W_j + band of Pair[.][d_j]).
 //
 // Roles.  Warp 0 (the "serial" warp) runs, per block, the part of Eq. 6 that is
 // inherently sequential: targets K0 < j <= k in the same block need C[.][j-1]
 // of the step before (the paper's barrier per step), done here in
-// registers with warp shuffles.  Warps 1-3 (the "rectangle" warps) compute,
-// for the NEXT block b+1 and while warp 0 works on block b, every cell whose
-// bottom j is already final: its 32 target rows, and bottoms j <= K0 in 32-row
-// chunks.  Only the newest chunk (bottoms of block b) waits for warp 0, and is
-// split two ways (warps 2-3 meanwhile precompute the next triangle).  The serial warp also finalises each target: ground and
-// sky running minima (their data term does not depend on the predecessor, so
-// GR^k = PG[k+1] + min_j (C_O[j-1] + t - PG[j])), the index table and
-// the 32-byte record of row k+1 that later rectangles read.
+// registers with warp shuffles; it also finalises each target -- ground and sky
+// running minima (their data term does not depend on the predecessor, so
+// GR^k = PG[k+1] + min_j (C_O[j-1] + t - PG[j])), the index table and the
+// 32-byte record of row k+1 that later rectangles read.  Meanwhile warp 1 builds
+// block b+1's priv rows and warps 1-3 (the "rectangle" warps) evaluate every
+// cell of block b+1's targets whose bottom is already final (j <= K0), in 32-row
+// chunks handed out dynamically; warp 0 joins them after its triangle.  Only the
+// newest chunk (bottoms of block b) waits for warp 0: warps 0-1 take 16 rows
+// each while warps 2-3 precompute block b+1's triangle cells.
 // Exact mode (L#22): all costs are integer quanta < 2^24 carried in fp32, so
 // adds/mins are exact and every decision matches the oracle.
 // ---------------------------------------------------------------------------
