@@ -5,15 +5,15 @@
 //                    P:207-219), the Eq. 5-6 min-plus DP (P:129-157,
 //                    P:221-235) and fused backtracking.
 //
-// Design: one WARP per column, lanes own targets k in
-// blocks of 32 ("lanes own targets"), bottoms j iterate warp-uniformly.  The
+// Design: a group of 4 warps per column, lanes own targets
+// k in blocks of 32 ("lanes own targets"), bottoms j iterate warp-uniformly.  The
 // object LUT LUT_object[f][v] (D x (h+1) per column, 220 KiB at 1024x440,
 // P:209 "too large to fit into Shared Memory") is never materialised: the 32
-// rows LUT[.][k+1] of the current target block live in shared memory ("priv"),
-// and the row LUT[.][j] of the current bottom is carried incrementally in a
-// 4-deep shared ring (row_{j+1} = row_j + Pair[.][d_j]).  Costs are fp32; in
-// exact mode (L#22) they are integer quanta < 2^24, so every add and min is
-// exact and decisions match the double-precision oracle bit for bit.
+// rows of the current target block live in shared memory ("priv"), and the row
+// of the current bottom is carried incrementally in per-warp buffers updated
+// only within the pair-cost band (row_{j+1} = row_j + Pair[.][d_j]).  Costs are
+// fp32; in exact mode (L#22) they are integer quanta < 2^24, so every add and
+// min is exact and decisions match the double-precision oracle bit for bit.
 #pragma once
 #include <cstdint>
 #include <type_traits>
