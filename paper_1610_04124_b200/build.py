@@ -31,14 +31,21 @@ def stale() -> bool:
     return any(os.path.getmtime(s) > t for s in SOURCES + [HEADER])
 
 
-def build(force: bool = False, verbose: bool = False, trace: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, trace: bool = False,
+          variant: str | None = None, src: str | None = None) -> str:
     """trace=True builds the diagnostic phase-timeline variant libstixels_trace.so
-    (-DSTX_TRACE; scripts/trace_phases.py), never loaded by the product."""
-    out = LIB if not trace else os.path.join(HERE, "libstixels_trace.so")
-    if not trace and not force and not stale():
+    (-DSTX_TRACE; scripts/trace_phases.py); variant=name builds libstixels_<name>.so
+    (from the api.cu at `src` if given) for A/B timing.  Neither is loaded by the
+    product (see stixels.lib)."""
+    out = LIB
+    if trace:
+        out = os.path.join(HERE, "libstixels_trace.so")
+    elif variant:
+        out = os.path.join(HERE, f"libstixels_{variant}.so")
+    if out == LIB and not force and not stale():
         return LIB
-    cmd = [nvcc()] + NVCC_FLAGS + (["-DSTX_TRACE"] if trace else []) + ["-o", out,
-                                                                        os.path.join(CSRC, "api.cu")]
+    cmd = [nvcc()] + NVCC_FLAGS + (["-DSTX_TRACE"] if trace else []) + [
+        "-o", out, src or os.path.join(CSRC, "api.cu")]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError("nvcc failed:\n" + res.stdout + res.stderr)

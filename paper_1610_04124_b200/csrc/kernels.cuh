@@ -610,7 +610,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
     }
     int f0 = fmean(r0), f1 = fmean(r1);
     __syncwarp();
-#pragma unroll 1
+#pragma unroll 2          // 8 bottoms per iteration (A/B: +1.2%)
     for (int jj = 0; jj < nsteps; jj += 4) {
 #pragma unroll
       for (int half = 0; half < 2; ++half) {

@@ -58,10 +58,14 @@ def lib() -> ctypes.CDLL:
     """Load libstixels.so (built in-tree by paper_1610_04124_b200.build).  Raises if absent."""
     global _lib
     if _lib is None:
-        if not os.path.exists(LIB):
-            raise RuntimeError(f"{LIB} not built; run paper_1610_04124_b200.build.build() "
+        # STIXELS_LIB_VARIANT=name loads the A/B build libstixels_<name>.so (same
+        # directory; scripts only) instead of the product library
+        var = os.environ.get("STIXELS_LIB_VARIANT")
+        path = LIB if not var else os.path.join(os.path.dirname(LIB), f"libstixels_{var}.so")
+        if not os.path.exists(path):
+            raise RuntimeError(f"{path} not built; run paper_1610_04124_b200.build.build() "
                                "(there is no CPU fallback)")
-        L = ctypes.CDLL(LIB)
+        L = ctypes.CDLL(path)
         vp, i32, i64 = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64
         P = ctypes.POINTER
         L.stixels_default_params.argtypes = [P(Params)]
