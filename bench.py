@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--e2e-batch", type=int, default=1024)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-single", action="store_true", help="skip the one-frame latency run")
     ap.add_argument("--cpu-frames", type=int, default=0, help="oracle sample size (0 = auto)")
     ap.add_argument("--sweep", action="store_true",
                     help="NEXT f1: resolution / stixel-width sweep with fps/W (one JSON line "
@@ -491,7 +492,7 @@ def main():
     # BASELINE configs[1]: ONE frame per call (latency; the GPU is mostly idle: 204
     # columns for 592 column slots), frames back to back, inputs resident
     single = None
-    if rank == 0:
+    if rank == 0 and not args.no_single:
         hd1 = S.Handle(params, W_IMG, H_IMG, 1, device=local, stream=stream)
         o1, c1, k1 = hd1.alloc_outputs(1)
         with torch.cuda.stream(stream):
