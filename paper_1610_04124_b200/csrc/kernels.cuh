@@ -270,8 +270,7 @@ struct DPArgs {
 
 struct ColSmem {
   float* priv;      // [32][DP+1]     priv[i][f] = LUT_object[f][32b+i+1] of the block being built
-  float* seed;      // [3][DP] W-row 32b of block b (slot b % 3: written by the build two
-                    // blocks ahead), then [2][DP] W-row 32b+16 (slot b & 1)
+  float* seed;      // [2][DP] W-row 32b+16 of block b (slot b & 1)
   float* ring;      // [4][ring_stride] per-warp W-rows W_j = LUT_object[.][j] - cap*j (RR = 2 sparse, 4 dense)
   float* cbd;       // [496]          triangle cells (bottom K0+1+j', target K0+k' > j'), packed:
                     //                object data term,
@@ -317,7 +316,7 @@ template <int DP, bool SPARSE>
 __host__ __device__ inline int col_smem_bytes(int h) {
   int b = 0;
   b += al16(32 * (DP + 1) * 4);
-  b += al16(5 * DP * 4);
+  b += al16(2 * DP * 4);
   b += al16(kCW * ring_stride<DP, SPARSE>() * 4);
   b += 2 * al16(kTri * 4) + al16(kTri * 2);
   b += al16((h + 3) * 32);
@@ -340,7 +339,7 @@ template <int DP, bool SPARSE>
 __device__ inline ColSmem carve(uint8_t* p, int h) {
   ColSmem w;
   w.priv = reinterpret_cast<float*>(p); p += al16(32 * (DP + 1) * 4);
-  w.seed = reinterpret_cast<float*>(p); p += al16(5 * DP * 4);
+  w.seed = reinterpret_cast<float*>(p); p += al16(2 * DP * 4);
   w.ring = reinterpret_cast<float*>(p); p += al16(kCW * ring_stride<DP, SPARSE>() * 4);
   w.cbd = reinterpret_cast<float*>(p); p += al16(kTri * 4);
   w.cbg = reinterpret_cast<float*>(p); p += al16(kTri * 4);
@@ -710,7 +709,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
       const uint32_t ehi = PAIR2D ? (uint32_t)(valid ? dr : a.D + 1) : (uint32_t)(dmr * 4);
       cs.eo[v] = (uint32_t)(cc * a.esz * 4 + (dmr - cc) * 4) | (ehi << 16);
     }
-    for (int i = ctid; i < DP; i += kCW * 32) { ANg[i] = 0.f; cs.seed[i] = 0.f; }   // W[.][0] = 0
+    for (int i = ctid; i < DP; i += kCW * 32) ANg[i] = 0.f;   // W[.][0] = 0
     if (ctid == 0) *cs.ctr = 0;
     named_bar(bar_col, kCW * 32);
     STX_STAMP(63, w);                    // clock calibration (all warps just released)
@@ -784,10 +783,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
         }
       }
 #pragma unroll
-      for (int c = 0; c < NS; ++c) {
-        ANg[(bt + 1) * DP + 32 * c + lane] = fr[c];
-        cs.seed[((bt + 1) % 3) * DP + 32 * c + lane] = fr[c];   // newest-chunk seed of block bt+1
-      }
+      for (int c = 0; c < NS; ++c) ANg[(bt + 1) * DP + 32 * c + lane] = fr[c];
     };
     // triangle cells of block bt: bottom K0+1+j', target K0+k' (k' > j'); their
     // bottoms' W-rows are the block's own priv rows: data term (absolute),
@@ -818,7 +814,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
     // seed of the second half of block bt's newest chunk: W-row K0 + 16 (priv row 15)
     auto copy_seed = [&](int bt) {
       if ((bt << 5) + 32 < h) {          // only needed if a next block exists
-        float* sd = cs.seed + (3 + (bt & 1)) * DP;
+        float* sd = cs.seed + (bt & 1) * DP;
         const float* row = cs.priv + 15 * (DP + 1);
         for (int f = lane; f < DP; f += 32) sd[f] = row[f];
       }
@@ -1034,6 +1030,9 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
         // full chunks m <= b-1: their records (rows <= 32 b) were final before block b
         bulk_chunks(b, ppn_s, Tn, N4n, rbest, rargj);
       }
+      // warp 0's newest-chunk seed W[.][K0] from L2, prefetched before the barrier
+      float rs0[4 * NR];
+      if (w == 0 && has_next) load_seed(rs0, ANg + b * DP);
       STX_STAMP(b, 3 + w);
       named_bar(bar_col, kCW * 32);
       if (w == 0) STX_STAMP(b, 7);
@@ -1043,7 +1042,12 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
         // warps 2 and 3 precompute block b+1's triangle cells
         if (w < 2) {
           float rr[4 * NR];
-          load_seed(rr, cs.seed + (w == 0 ? b % 3 : 3 + (b & 1)) * DP);   // W-rows K0, K0+16
+          if (w == 0) {
+#pragma unroll
+            for (int i = 0; i < 4 * NR; ++i) rr[i] = rs0[i];
+          } else {
+            load_seed(rr, cs.seed + (b & 1) * DP);                           // W-row K0+16
+          }
           rect_run(rr, K0 + 1 + 16 * w, 16, ppn_s, Tn, N4n, rbest, rargj);
         } else {
           precompute_cells(bn, ctid - 64, 64);
