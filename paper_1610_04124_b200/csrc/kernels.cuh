@@ -270,13 +270,12 @@ struct DPArgs {
 
 struct ColSmem {
   float* priv;      // [32][DP+1]     priv[i][f] = LUT_object[f][32b+i+1] of the block being built
-  uint64_t* mbar;   // [4]            record groups of the block being finalised (rows K0+1+8g ..
-                    //                K0+8+8g published by the serial warp's chain, mbarrier g)
+  float* seed;      // [2][DP] W-row 32b+16 of block b (slot b & 1)
   float* ring;      // [4][ring_stride] per-warp W-rows W_j = LUT_object[.][j] - cap*j (RR = 2 sparse, 4 dense)
-  float* cbd;       // [496]          triangle cells (bottom K0+1+j', target K0+k' > j'), packed:
-                    //                object data term,
-  float* cbg;       // [496]          ... the same plus its O-above-G prior (gravity level),
-  uint16_t* cbf;    // [496]          ... and the object mean f
+  float4* cell;     // [496]          triangle cells (bottom K0+1+j', target K0+k' > j'), one
+                    //                16-byte record each (one LDS.128 in the serial chain):
+                    //                {object data term, the same plus its O-above-G prior
+                    //                (gravity level), object mean f (int bits), unused}
   uint4* rec;       // [h+3][2]       row j: {AO0,AO1,AGm,AGh} {AGl, T[j], N4[j], ordthr | drp<<16}
   uint2* tn;        // [h+1]          row j: {T[j], N4[j]} (compact copy for per-lane rows)
   uint32_t* eo;     // [h+2]          lo16: ring window byte offset; hi16: E0 byte offset
@@ -317,9 +316,9 @@ template <int DP, bool SPARSE>
 __host__ __device__ inline int col_smem_bytes(int h) {
   int b = 0;
   b += al16(32 * (DP + 1) * 4);
-  b += 32;
+  b += al16(2 * DP * 4);
   b += al16(kCW * ring_stride<DP, SPARSE>() * 4);
-  b += 2 * al16(kTri * 4) + al16(kTri * 2);
+  b += kTri * 16;
   b += al16((h + 3) * 32);
   b += al16((h + 1) * 8);
   b += al16((h + 2) * 4);
@@ -340,11 +339,9 @@ template <int DP, bool SPARSE>
 __device__ inline ColSmem carve(uint8_t* p, int h) {
   ColSmem w;
   w.priv = reinterpret_cast<float*>(p); p += al16(32 * (DP + 1) * 4);
-  w.mbar = reinterpret_cast<uint64_t*>(p); p += 32;
+  w.seed = reinterpret_cast<float*>(p); p += al16(2 * DP * 4);
   w.ring = reinterpret_cast<float*>(p); p += al16(kCW * ring_stride<DP, SPARSE>() * 4);
-  w.cbd = reinterpret_cast<float*>(p); p += al16(kTri * 4);
-  w.cbg = reinterpret_cast<float*>(p); p += al16(kTri * 4);
-  w.cbf = reinterpret_cast<uint16_t*>(p); p += al16(kTri * 2);
+  w.cell = reinterpret_cast<float4*>(p); p += kTri * 16;
   w.rec = reinterpret_cast<uint4*>(p); p += al16((h + 3) * 32);
   w.tn = reinterpret_cast<uint2*>(p); p += al16((h + 1) * 8);
   w.eo = reinterpret_cast<uint32_t*>(p); p += al16((h + 2) * 4);
@@ -382,23 +379,6 @@ __device__ __forceinline__ float opaque(float x) { return __shfl_sync(0xffffffff
 
 __device__ __forceinline__ void named_bar(int id, int threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
-}
-
-// Shared-memory mbarriers (one phase per block): the serial warp's 32 lanes
-// arrive (release their record stores), consumers wait on the phase parity.
-__device__ __forceinline__ void mbar_init(uint32_t a, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint32_t a) {
-  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}" ::"r"(a) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n"
-      "STX_MBAR_WAIT:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra STX_MBAR_WAIT;\n"
-      "}" ::"r"(a), "r"(parity) : "memory");
 }
 
 constexpr int kM2Pad = 16;          // bytes of shared memory before the M2 table
@@ -578,10 +558,8 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
   const uint32_t m2_s = (uint32_t)__cvta_generic_to_shared(M2s);   // (dynamic smem does not start at 0)
   const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ringw) + ring_b0<DP, SPARSE>();
   const uint32_t bbuf_s = ring_s + ((lane < 16) ? ring_b1<DP, SPARSE>() : 0u) + (uint32_t)((boff - 1) * 4);
-  // seed = false continues the previous run of this warp (j0 = its last j + 1): the
-  // W-row buffers already hold W_{j0} / W_{j0+1} (they depend only on the input).
   auto rect_run = [&](float (&rr)[4 * NR], int j0, int nsteps, uint32_t pp_s, uint32_t Tk,
-                      uint32_t N4k, float& best, int& argj, bool seed) {
+                      uint32_t N4k, float& best, int& argj) {
     // sparse band round: f = drp - 1 + boff always lands in the buffer or its
     // guards (no range test; zero-weight lanes write back their value)
     auto band = [&](int drpA, int drpB) {
@@ -610,8 +588,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
       return (int)__umulhi((Tk - r.T) >> (kRBits - 1), M);   // < D: inputs below D - 1/2 (L#27)
     };
     RowU r0 = rowj(j0), r1 = rowj(j0 + 1);
-    if (!seed) {
-    } else if constexpr (SPARSE) {
+    if constexpr (SPARSE) {
       // both buffers := W_{j0-1}; then buffer 1 = W_{j0}, buffer 0 = W_{j0+1}
       const int drm = rowj(j0 - 1).drp;
 #pragma unroll
@@ -661,43 +638,31 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
       }
     }
   };
-  // Full 32-row chunks m < mend for this warp's targets, handed out dynamically
-  // (counter values base + m); the anchor row of the next chunk is prefetched from
-  // L2 while one runs.  Every warp leaves with the first index it drew that is
-  // >= mend (returned; so each step draws exactly mend + kCW values): index mend is
-  // the newest chunk, whose seed W-row W[.][32 mend] is then in rr.
-  auto bulk_chunks = [&](int mend, int base, float (&rr)[4 * NR], uint32_t pp_s, uint32_t Tk,
-                         uint32_t N4k, float& best, int& argj) -> int {
-    auto draw = [&]() {
-      int m = 0;
-      if (lane == 0) m = atomicAdd(cs.ctr, 1);
-      return __shfl_sync(0xffffffffu, m, 0) - base;
-    };
-    int m = draw();
-    if (m <= mend) load_seed(rr, ANg + m * DP);
+  // Full 32-row chunks m < mend for this warp's targets, handed out dynamically;
+  // the anchor row of the next chunk is prefetched from L2 while one runs.
+  auto bulk_chunks = [&](int mend, uint32_t pp_s, uint32_t Tk, uint32_t N4k, float& best,
+                         int& argj) {
+    int m = 0;
+    if (lane == 0) m = atomicAdd(cs.ctr, 1);
+    m = __shfl_sync(0xffffffffu, m, 0);
+    float rr[4 * NR];
+    if (m < mend) load_seed(rr, ANg + m * DP);
     while (m < mend) {
-      const int m2 = draw();
+      int m2 = 0;
+      if (lane == 0) m2 = atomicAdd(cs.ctr, 1);
+      m2 = __shfl_sync(0xffffffffu, m2, 0);
       float nx[4 * NR];
 #pragma unroll
       for (int i = 0; i < 4 * NR; ++i) nx[i] = 0.f;
-      if (m2 <= mend) load_seed(nx, ANg + m2 * DP);
-      rect_run(rr, 32 * m + 1, 32, pp_s, Tk, N4k, best, argj, true);
+      if (m2 < mend) load_seed(nx, ANg + m2 * DP);
+      rect_run(rr, 32 * m + 1, 32, pp_s, Tk, N4k, best, argj);
 #pragma unroll
       for (int i = 0; i < 4 * NR; ++i) rr[i] = nx[i];
       m = m2;
     }
-    return m;
   };
 
   float fr[NS];                        // builder warp: W[f][32 bt] for f = lane + 32c
-
-  // record-group mbarriers: 32 arrivals (the serial warp) complete a phase; one
-  // phase per block that has a next block, counted by every warp in nph
-  const uint32_t mb_s = (uint32_t)__cvta_generic_to_shared(cs.mbar);
-  if (ctid == 0)
-    for (int g = 0; g < 4; ++g) mbar_init(mb_s + 8u * g, 32);
-  named_bar(bar_col, kCW * 32);
-  uint32_t nph = 0;
 
   bool first_item = true;
   (void)first_item;
@@ -821,6 +786,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
     // triangle cells of block bt: bottom K0+1+j', target K0+k' (k' > j'); their
     // bottoms' W-rows are the block's own priv rows: data term (absolute),
     // f, gravity level.  The 496 cells are spread densely over the column group.
+    // Also keeps the W-rows K0+8, K0+16, K0+24 as seeds of block bt+1's newest chunk.
     auto precompute_cells = [&](int bt, int t0, int nthr) {
       const int K0b = bt << 5;
       const int jn = min(K0b + 31, h - 1) - K0b;
@@ -837,23 +803,18 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
           // thresholds from the constant bank: a warp's cells span one or two rows
           const int jr = K0b + jp + 1;
           const float pen = (f >= a.thrA1[jr]) ? a.kGO_hi : ((f < a.thrB[jr]) ? a.kGO_lo : a.kGO_mid);
-          cs.cbd[idx] = data;
-          cs.cbg[idx] = data + pen;
-          cs.cbf[idx] = (uint16_t)f;
+          cs.cell[idx] = make_float4(data, data + pen, __int_as_float(f), 0.f);
         }
       }
     };
-    // record of row k+1 (consumed by later rectangles): predecessor terms of
-    // C_O[k] (object mean f) and C_G[k], shifted by -cap*(k+1)
-    auto write_rec = [&](int k, float co, int f, float cg) {
-      const float sh = capQ * (float)(k + 1);
-      cs.rec[2 * (k + 1)] = make_uint4(__float_as_uint((co + a.kOO_lo) - sh), __float_as_uint((co + a.kOO_hi) - sh),
-                                       __float_as_uint((cg + a.kGO_mid) - sh), __float_as_uint((cg + a.kGO_hi) - sh));
-      uint32_t* ry = reinterpret_cast<uint32_t*>(cs.rec + 2 * (k + 1) + 1);
-      ry[0] = __float_as_uint((cg + a.kGO_lo) - sh);
-      reinterpret_cast<uint16_t*>(ry + 3)[0] = (uint16_t)(f + a.ord_margin);   // ordthr (drp kept)
+    // seed of the second half of block bt's newest chunk: W-row K0 + 16 (priv row 15)
+    auto copy_seed = [&](int bt) {
+      if ((bt << 5) + 32 < h) {          // only needed if a next block exists
+        float* sd = cs.seed + (bt & 1) * DP;
+        const float* row = cs.priv + 15 * (DP + 1);
+        for (int f = lane; f < DP; f += 32) sd[f] = row[f];
+      }
     };
-    int cbase = 0;                       // chunk counter value at the start of the step
 
     if (w == 1) {
 #pragma unroll
@@ -877,6 +838,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
       }
       cs.part[w * 32 + lane] = make_float2(rbest, __int_as_float(rargj));
       precompute_cells(0, ctid, kCW * 32);
+      if (w == 2) copy_seed(0);
     }
     named_bar(bar_col, kCW * 32);
 
@@ -942,25 +904,17 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
         float rB = __shfl_sync(0xffffffffu, best, 1);
         int rF = __shfl_sync(0xffffffffu, argf, 1);
         int off = 0;                                    // tri_off(jp)
-        float cgm = prevCG;                             // C_G[k] of this lane's row (lane 0: C_G[K0])
         STX_STAMP(b, 13);                 // serial: merge + recovery + chain setup done
-        // the chain in 4 segments ending at steps 6, 14, 22, 30: after step 8g+6 rows
-        // K0..K0+8g+7 are final (lane 8g+7's diagonal was that step), so records
-        // K0+8g+1 .. K0+8g+8 are published for the consumer of block b+1's newest
-        // chunk (a block with a next block is full: jn = 31)
-        int jp = 0;
-#pragma unroll 1
-        for (int g = 0; g < 4; ++g) {
-         const int jend = min(jn, 8 * g + 7);
-         for (; jp < jend; ++jp) {
+        for (int jp = 0; jp < jn; ++jp) {
           const int j = K0 + jp + 1;                    // bottom j; target j finalised
           const float4 q = cs.pgps[jp + 1];
           // diagonal cell (bottom j, target j), evaluated redundantly by all lanes
           // (data + min(aO, aG) computed as min(data + aO, (data + pen) + C_G): the
           // same value, exactly so in exact mode (integer quanta))
-          const float dd = cs.cbd[off];
-          const float dg = cs.cbg[off];
-          const int df = cs.cbf[off];
+          const float4 dcell = cs.cell[off];
+          const float dd = dcell.x;
+          const float dg = dcell.y;
+          const int df = __float_as_int(dcell.z);
           const float daO = prevCO + ((df > prevF + om) ? oh : ol);
           const float dc = fminf(dd + daO, dg + prevCG);
           const bool take = dc < rB;
@@ -969,9 +923,10 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
           // this lane's cell (bottom j, target k > j) with the same predecessors
           {
             const int idx = off + lane - jp - 1;        // (lanes <= jp read a dead slot)
-            const float data = cs.cbd[idx];
-            const float dgl = cs.cbg[idx];
-            const int f = cs.cbf[idx];
+            const float4 lc = cs.cell[idx];
+            const float data = lc.x;
+            const float dgl = lc.y;
+            const int f = __float_as_int(lc.z);
             const float tO = data + (prevCO + ((f > prevF + om) ? oh : ol));
             const float tG = dgl + prevCG;
             const bool pg = tG <= tO;                   // == (aG <= aO): data added to both
@@ -987,15 +942,9 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
           // ground: GR^j = PG[j+1] + min(.., C_O[j-1] + t - PG[j])  (value only)
           mg = fminf(mg, prevCO + q.x);
           prevCG = q.y + mg;
-          cgm = (lane == jp + 1) ? prevCG : cgm;
           prevCO = COj;
           prevF = Fj;
           off += 31 - jp;
-         }
-         if (has_next) {
-           if ((lane >> 3) == g) write_rec(k, best, argf, cgm);
-           mbar_arrive(mb_s + 8u * (uint32_t)g);
-         }
         }
         STX_STAMP(b, 14);                 // serial: triangle chain done
         // ---- ground / sky argmins and values of the block's rows, as warp scans ----
@@ -1038,9 +987,16 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
           lastO = cCO; lastG = cCG; lastS = __shfl_sync(0xffffffffu, CSk, L);
         }
         STX_STAMP(b, 15);                 // serial: scans + carries done
-        // every lane now holds the final values of its target row k: the index
-        // table (its record was published during the chain)
+        // every lane now holds the final values of its target row k: write the
+        // record of row k+1 (consumed by later rectangles; predecessor terms
+        // shifted by -cap*(k+1)) and the index table
         if (k < h) {
+          const float sh = capQ * (float)(k + 1);
+          cs.rec[2 * (k + 1)] = make_uint4(__float_as_uint((best + a.kOO_lo) - sh), __float_as_uint((best + a.kOO_hi) - sh),
+                                           __float_as_uint((CGk + a.kGO_mid) - sh), __float_as_uint((CGk + a.kGO_hi) - sh));
+          uint32_t* ry = reinterpret_cast<uint32_t*>(cs.rec + 2 * (k + 1) + 1);
+          ry[0] = __float_as_uint((CGk + a.kGO_lo) - sh);
+          reinterpret_cast<uint16_t*>(ry + 3)[0] = (uint16_t)(argf + a.ord_margin);   // ordthr (drp kept)
           cs.argO[k] = (uint16_t)(argj | (argc << 12));
           cs.argG[k] = (uint16_t)aG;
           cs.argS[k] = (uint16_t)aS;
@@ -1070,26 +1026,33 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
           rargj = 0;
         }
         // full chunks m <= b-1: their records (rows <= 32 b) were final before block b
-        float rr[4 * NR];
-        const int mt = bulk_chunks(b, cbase, rr, ppn_s, Tn, N4n, rbest, rargj);
-        STX_STAMP(b, 3 + w);
-        const uint32_t par = nph & 1u;
-        if (mt == b) {
-          // newest chunk (bottoms K0+1 .. K0+32): streamed in groups of 8 bottoms as
-          // the serial warp's chain publishes their records, one W-row run
-#pragma unroll 1
-          for (int g = 0; g < 4; ++g) {
-            mbar_wait(mb_s + 8u * (uint32_t)g, par);
-            rect_run(rr, K0 + 1 + 8 * g, 8, ppn_s, Tn, N4n, rbest, rargj, g == 0);
+        bulk_chunks(b, ppn_s, Tn, N4n, rbest, rargj);
+      }
+      // warp 0's newest-chunk seed W[.][K0] from L2, prefetched before the barrier
+      float rs0[4 * NR];
+      if (w == 0 && has_next) load_seed(rs0, ANg + b * DP);
+      STX_STAMP(b, 3 + w);
+      named_bar(bar_col, kCW * 32);
+      if (w == 0) STX_STAMP(b, 7);
+      if (has_next) {
+        // newest chunk (bottoms K0+1 .. K0+32, final after block b's triangle):
+        // warps 0 and 1 take 16 rows each, seeded from W-rows K0 and K0+16, while
+        // warps 2 and 3 precompute block b+1's triangle cells
+        if (w < 2) {
+          float rr[4 * NR];
+          if (w == 0) {
+#pragma unroll
+            for (int i = 0; i < 4 * NR; ++i) rr[i] = rs0[i];
+          } else {
+            load_seed(rr, cs.seed + (b & 1) * DP);                           // W-row K0+16
           }
-        } else if (mt <= b + 2) {
-          // block b+1's triangle cells, once block b's chain no longer reads them
-          mbar_wait(mb_s + 24u, par);
-          precompute_cells(bn, 32 * (mt - b - 1) + lane, 64);
+          rect_run(rr, K0 + 1 + 16 * w, 16, ppn_s, Tn, N4n, rbest, rargj);
+        } else {
+          precompute_cells(bn, ctid - 64, 64);
+          if (w == 2) copy_seed(bn);
         }
         cs.part[w * 32 + lane] = make_float2(rbest, __int_as_float(rargj));
-        cbase += b + kCW;
-        ++nph;
+        if (ctid == 0) *cs.ctr = 0;
       }
       STX_STAMP(b, 8 + w);
       named_bar(bar_col, kCW * 32);
