@@ -548,23 +548,35 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
 #pragma unroll
       for (int c = 0; c < 4; ++c) rr[4 * r + c] = row[4 * lane + 128 * r + c];
   };
-  // Bottoms j0 .. j0+nsteps-1 (j0 = 1 mod 4, nsteps = 0 mod 4) for this warp's
-  // targets (priv row at shared address pp_s); rr holds the W-row W[.][j0-1].
+  // Bottoms j0 .. j0+nsteps-1 (j0 = 1 mod 4, nsteps = 0 mod 4) for this warp's 32
+  // targets; rr holds the W-row W[.][j0-1].  Lanes hold target PAIRS: lane l owns
+  // targets t0 = l & 15 and t1 = t0 + 16 of the block, and half-warp hw = l >> 4
+  // takes bottom jA + hw of each bottom pair (jA, jA+1).  So a lane loads one row
+  // record (and its gravity thresholds) per pair and uses it for two cells: the
+  // per-row work, which costs a warp instruction per 32 cells when lanes own one
+  // target each, is halved per cell.  The two halves' running minima of a target
+  // (odd / even bottoms) are merged at the end of the step (merge_part).
   // Candidates are shifted by -cap*(k+1):  (P_k - W_j)[f] + min(aO', aG').
-  // Software-pipelined: the next pair's records and object means are computed
+  // Software-pipelined: the next pair's record and object means are computed
   // before the current pair's table loads.  Shared memory is addressed with
   // explicit 32-bit offsets.
+  struct Tg { uint32_t pp0, pp1, T0, T1, N0, N1; };   // priv rows, T[k+1], N4[k+1] of t0 / t1
+  struct Acc { float b0, b1; int a0, a1; };           // running minima {cost, argj} of t0 / t1
+  const int hw = lane >> 4;
   const uint32_t rec_s = (uint32_t)__cvta_generic_to_shared(cs.rec);
   const uint32_t m2_s = (uint32_t)__cvta_generic_to_shared(M2s);   // (dynamic smem does not start at 0)
   const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ringw) + ring_b0<DP, SPARSE>();
-  const uint32_t bbuf_s = ring_s + ((lane < 16) ? ring_b1<DP, SPARSE>() : 0u) + (uint32_t)((boff - 1) * 4);
-  auto rect_run = [&](float (&rr)[4 * NR], int j0, int nsteps, uint32_t pp_s, uint32_t Tk,
-                      uint32_t N4k, float& best, int& argj) {
+  // band rounds: round 1 lanes 0-14 -> buffer 1, lanes 16-30 -> buffer 0; round 2
+  // the other way round (each half applies a pixel of its own row records)
+  const uint32_t bbuf1_s = ring_s + ((lane < 16) ? ring_b1<DP, SPARSE>() : 0u) + (uint32_t)((boff - 1) * 4);
+  const uint32_t bbuf2_s = ring_s + ((lane < 16) ? 0u : ring_b1<DP, SPARSE>()) + (uint32_t)((boff - 1) * 4);
+  // the W-row this half reads: buffer 1 holds W_jA (half 0), buffer 0 W_{jA+1} (half 1)
+  const uint32_t wbuf_s = ring_s + ((lane < 16) ? ring_b1<DP, SPARSE>() : 0u);
+  auto rect_run = [&](float (&rr)[4 * NR], int j0, int nsteps, const Tg& tg, Acc& acc) {
     // sparse band round: f = drp - 1 + boff always lands in the buffer or its
     // guards (no range test; zero-weight lanes write back their value)
-    auto band = [&](int drpA, int drpB) {
-      const int drp = (lane < 16) ? drpA : drpB;
-      float* q = shp<float>(bbuf_s + 4u * (uint32_t)drp);
+    auto band = [&](uint32_t base, int drp) {
+      float* q = shp<float>(base + 4u * (uint32_t)drp);
       if constexpr (PAIR2D) {
         const float wgt = *shp<const float>(wt_s + 64u * (uint32_t)drp);
         if (blive) *q -= wgt;
@@ -576,72 +588,83 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
       const uint4* q = shp<const uint4>(rec_s + 32u * (uint32_t)j);
       return unpack_row(q[0], q[1]);
     };
-    auto cell = [&](const RowU& r, int j, int f, float pw) {
+    auto cell = [&](const RowU& r, int j, int thA, int thB, int f, float pw, float& best, int& argj) {
       float aO = (f > r.ordthr) ? r.AO1 : r.AO0;
-      float aG = (f >= a.thrA1[j]) ? r.AGh : ((f < a.thrB[j]) ? r.AGl : r.AGm);
+      float aG = (f >= thA) ? r.AGh : ((f < thB) ? r.AGl : r.AGm);
       float cand = pw + fminf(aO, aG);
       if (cand < best) { best = cand; argj = j; }
     };
-    auto fmean = [&](const RowU& r) {
+    auto fmean = [&](const RowU& r, uint32_t Tk, uint32_t N4k) {
       const uint32_t n4 = N4k - r.N4;
       const uint32_t M = *shp<const uint32_t>(m2_s + n4);
       return (int)__umulhi((Tk - r.T) >> (kRBits - 1), M);   // < D: inputs below D - 1/2 (L#27)
     };
-    RowU r0 = rowj(j0), r1 = rowj(j0 + 1);
+    RowU r = rowj(j0 + hw);
     if constexpr (SPARSE) {
       // both buffers := W_{j0-1}; then buffer 1 = W_{j0}, buffer 0 = W_{j0+1}
       const int drm = rowj(j0 - 1).drp;
 #pragma unroll
-      for (int r = 0; r < NR; ++r) {
-        const float4 v = make_float4(rr[4 * r], rr[4 * r + 1], rr[4 * r + 2], rr[4 * r + 3]);
-        *shp<float4>(ring_s + 16u * lane + 512u * r) = v;
-        *shp<float4>(ring_s + ring_b1<DP, SPARSE>() + 16u * lane + 512u * r) = v;
+      for (int q = 0; q < NR; ++q) {
+        const float4 v = make_float4(rr[4 * q], rr[4 * q + 1], rr[4 * q + 2], rr[4 * q + 3]);
+        *shp<float4>(ring_s + 16u * lane + 512u * q) = v;
+        *shp<float4>(ring_s + ring_b1<DP, SPARSE>() + 16u * lane + 512u * q) = v;
       }
       __syncwarp();
-      band(drm, drm);
+      band(bbuf1_s, drm);                       // both buffers += pixel j0-1
       __syncwarp();
-      band(kNoBand, r0.drp);
+      band(bbuf2_s, hw ? kNoBand : r.drp);      // buffer 0 += pixel j0 (half 0's row)
     } else {
       ring_step(rr, j0 - 1, 1);
       ring_step(rr, j0, 2);
     }
-    int f0 = fmean(r0), f1 = fmean(r1);
+    int f0 = fmean(r, tg.T0, tg.N0), f1 = fmean(r, tg.T1, tg.N1);
     __syncwarp();
-#pragma unroll 2          // 8 bottoms per iteration (A/B: +1.2%)
+#pragma unroll 2          // 8 bottoms per iteration
     for (int jj = 0; jj < nsteps; jj += 4) {
 #pragma unroll
       for (int half = 0; half < 2; ++half) {
         const int jA = j0 + jj + 2 * half;          // odd
-        // next pair (rows jA+2, jA+3).  After the run's last row jl <= k these are
-        // at most rows k+2, k+3 (<= h+2): their mean lookup reads M2 at n4 >= -8
-        // (inside the pad before M2) and is never used.
-        const RowU n0 = rowj(jA + 2), n1 = rowj(jA + 3);
-        const int g0 = fmean(n0), g1 = fmean(n1);
-        const uint32_t ra = SPARSE ? ring_s + ring_b1<DP, SPARSE>() : ring_s + ((1 + 2 * half) & 3) * DP * 4u;
-        const uint32_t rb = SPARSE ? ring_s : ring_s + ((2 + 2 * half) & 3) * DP * 4u;
-        const float p0 = *shp<const float>(pp_s + 4u * f0), p1 = *shp<const float>(pp_s + 4u * f1);
-        const float w0 = *shp<const float>(ra + 4u * f0), w1 = *shp<const float>(rb + 4u * f1);
-        cell(r0, jA, f0, p0 - w0);
-        cell(r1, jA + 1, f1, p1 - w1);
+        const int jm = jA + hw;                     // this half's bottom
+        // next pair (row jm+2).  After the run's last row jl <= k these are at most
+        // rows k+2, k+3 (<= h+2): their mean lookup reads M2 at n4 >= -8 (inside the
+        // pad before M2) and is never used.
+        const RowU n = rowj(jm + 2);
+        const int g0 = fmean(n, tg.T0, tg.N0), g1 = fmean(n, tg.T1, tg.N1);
+        const int thA = a.thrA1[jm], thB = a.thrB[jm];
+        const uint32_t wb = SPARSE ? wbuf_s : ring_s + (hw ? ((2 + 2 * half) & 3) : ((1 + 2 * half) & 3)) * DP * 4u;
+        const float p0 = *shp<const float>(tg.pp0 + 4u * f0), p1 = *shp<const float>(tg.pp1 + 4u * f1);
+        const float w0 = *shp<const float>(wb + 4u * f0), w1 = *shp<const float>(wb + 4u * f1);
+        cell(r, jm, thA, thB, f0, p0 - w0, acc.b0, acc.a0);
+        cell(r, jm, thA, thB, f1, p1 - w1, acc.b1, acc.a1);
         if constexpr (SPARSE) {
-          // buffer 1: W_jA -> W_{jA+2}; buffer 0: W_{jA+1} -> W_{jA+3}
+          // buffer 1: W_jA -> W_{jA+2} (pixels jA: half 0, jA+1: half 1);
+          // buffer 0: W_{jA+1} -> W_{jA+3} (pixels jA+1: half 1, jA+2: half 0's next row)
           __syncwarp();
-          band(r0.drp, r1.drp);
+          band(bbuf1_s, r.drp);
           __syncwarp();
-          band(r1.drp, n0.drp);
+          band(bbuf2_s, hw ? r.drp : n.drp);
         } else {
           ring_step(rr, jA + 1, (3 + 2 * half) & 3);
           ring_step(rr, jA + 2, (4 + 2 * half) & 3);
         }
-        r0 = n0; r1 = n1; f0 = g0; f1 = g1;
+        r = n; f0 = g0; f1 = g1;
         __syncwarp();
       }
     }
   };
+  // The step's result of target lane (t = lane): the two halves' minima merged,
+  // ties to the lower bottom (the first in bottom order, L#17).
+  auto merge_part = [&](const Acc& acc) {
+    const float sb = __shfl_xor_sync(0xffffffffu, hw ? acc.b0 : acc.b1, 16);
+    const int sa = __shfl_xor_sync(0xffffffffu, hw ? acc.a0 : acc.a1, 16);
+    float mb = hw ? acc.b1 : acc.b0;
+    int ma = hw ? acc.a1 : acc.a0;
+    if (sb < mb || (sb == mb && sa < ma)) { mb = sb; ma = sa; }
+    return make_float2(mb, __int_as_float(ma));
+  };
   // Full 32-row chunks m < mend for this warp's targets, handed out dynamically;
   // the anchor row of the next chunk is prefetched from L2 while one runs.
-  auto bulk_chunks = [&](int mend, uint32_t pp_s, uint32_t Tk, uint32_t N4k, float& best,
-                         int& argj) {
+  auto bulk_chunks = [&](int mend, const Tg& tg, Acc& acc) {
     int m = 0;
     if (lane == 0) m = atomicAdd(cs.ctr, 1);
     m = __shfl_sync(0xffffffffu, m, 0);
@@ -655,7 +678,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
 #pragma unroll
       for (int i = 0; i < 4 * NR; ++i) nx[i] = 0.f;
       if (m2 < mend) load_seed(nx, ANg + m2 * DP);
-      rect_run(rr, 32 * m + 1, 32, pp_s, Tk, N4k, best, argj);
+      rect_run(rr, 32 * m + 1, 32, tg, acc);
 #pragma unroll
       for (int i = 0; i < 4 * NR; ++i) rr[i] = nx[i];
       m = m2;
@@ -1011,22 +1034,23 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
         asm volatile("bar.arrive %0, %1;" ::"r"(bar_x), "r"(kCW * 32) : "memory");
       }
       // ======== all warps: block b+1, bottoms final before block b ===============
-      float rbest = INF;
-      int rargj = 0x7fffffff;
-      uint32_t Tn = 0, N4n = 0;
-      const float* ppn = cs.priv + lane * (DP + 1);
-      const uint32_t ppn_s = (uint32_t)__cvta_generic_to_shared(ppn);
+      Acc acc{INF, INF, 0x7fffffff, 0x7fffffff};
+      Tg tg{};
       if (has_next) {
-        const int kk = Kn + lane < h ? Kn + lane : h - 1;
-        const uint2 rky = cs.tn[kk + 1];
-        Tn = rky.x; N4n = rky.y;
-        if (w == 1) {                  // j = 0: first stixel spans 0..k (Eq. 5)
-          int f = span_f(Tn, N4n, smem, Dm1);
-          rbest = ppn[f] + a.piFirstO;
-          rargj = 0;
+        // this lane's target pair t0 = lane & 15, t1 = t0 + 16 of block b+1
+        const int t0 = lane & 15, t1 = t0 + 16;
+        const uint2 r0 = cs.tn[min(Kn + t0, h - 1) + 1], r1 = cs.tn[min(Kn + t1, h - 1) + 1];
+        const float* pp0 = cs.priv + t0 * (DP + 1);
+        const float* pp1 = cs.priv + t1 * (DP + 1);
+        tg = Tg{(uint32_t)__cvta_generic_to_shared(pp0), (uint32_t)__cvta_generic_to_shared(pp1),
+                r0.x, r1.x, r0.y, r1.y};
+        if (w == 1 && hw == 0) {       // j = 0: first stixel spans 0..k (Eq. 5)
+          acc.b0 = pp0[span_f(r0.x, r0.y, smem, Dm1)] + a.piFirstO;
+          acc.b1 = pp1[span_f(r1.x, r1.y, smem, Dm1)] + a.piFirstO;
+          acc.a0 = acc.a1 = 0;
         }
         // full chunks m <= b-1: their records (rows <= 32 b) were final before block b
-        bulk_chunks(b, ppn_s, Tn, N4n, rbest, rargj);
+        bulk_chunks(b, tg, acc);
       }
       // warp 0's newest-chunk seed W[.][K0] from L2, prefetched before the barrier
       float rs0[4 * NR];
@@ -1046,12 +1070,12 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
           } else {
             load_seed(rr, cs.seed + (b & 1) * DP);                           // W-row K0+16
           }
-          rect_run(rr, K0 + 1 + 16 * w, 16, ppn_s, Tn, N4n, rbest, rargj);
+          rect_run(rr, K0 + 1 + 16 * w, 16, tg, acc);
         } else {
           precompute_cells(bn, ctid - 64, 64);
           if (w == 2) copy_seed(bn);
         }
-        cs.part[w * 32 + lane] = make_float2(rbest, __int_as_float(rargj));
+        cs.part[w * 32 + lane] = merge_part(acc);
         if (ctid == 0) *cs.ctr = 0;
       }
       STX_STAMP(b, 8 + w);
