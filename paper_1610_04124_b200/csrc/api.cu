@@ -436,7 +436,8 @@ int stixels_create(const stixels_params* params, int width, int height, int max_
                       : (sparse ? col_smem_bytes<256, true>(height) : col_smem_bytes<256, false>(height));
   int sb = stx::kM2Pad + al16((height + 1) * 4) + (sparse ? stx::e_copies<true>() : stx::e_copies<false>()) * esz * 4 +
            al16(kTri * 2) +   // pad, M2, E copies, triangle decode
-           (pair2d ? (DPv + 17) * 16 * 4 : 0);   // NEXT f2 band weights
+           (pair2d ? (DPv + 17) * 16 * 4 : 0) +  // NEXT f2 band weights
+           al16(height * 8);                     // gravity thresholds per row
   int cpc = std::min(4, (optin - sb) / cb);   // columns per CTA (4 warps each)
   if (cpc < 1) return bail(STIXELS_ERR_UNSUPPORTED, "per-column shared memory exceeds the SM");
   h->cols_per_cta = cpc;

@@ -504,6 +504,10 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
   float* WT = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(tri_jk) + al16(kTri * 2));
   if constexpr (PAIR2D)
     for (int i = threadIdx.x; i < wt_rows<DP>() * 16; i += blockDim.x) WT[i] = a.WTg[i];
+  // gravity thresholds {thrA1[j], thrB[j]} per row (one LDS.64 per row in the rectangle)
+  int2* thrS = reinterpret_cast<int2*>(reinterpret_cast<uint8_t*>(WT) + (PAIR2D ? wt_rows<DP>() * 16 * 4 : 0));
+  for (int i = threadIdx.x; i < h; i += blockDim.x) thrS[i] = make_int2(a.thrA1[i], a.thrB[i]);
+  const uint32_t thr_s = (uint32_t)__cvta_generic_to_shared(thrS);
   for (int jp = 0; jp < 31; ++jp)                 // triangle cell index -> (j', k')
     for (int kp = jp + 1 + (int)threadIdx.x; kp < 32; kp += blockDim.x)
       tri_jk[tri_off(jp) + kp - jp - 1] = (uint16_t)(jp | (kp << 8));
@@ -630,7 +634,8 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
         // pad before M2) and is never used.
         const RowU n = rowj(jm + 2);
         const int g0 = fmean(n, tg.T0, tg.N0), g1 = fmean(n, tg.T1, tg.N1);
-        const int thA = a.thrA1[jm], thB = a.thrB[jm];
+        const int2 th = *shp<const int2>(thr_s + 8u * (uint32_t)jm);
+        const int thA = th.x, thB = th.y;
         const uint32_t wb = SPARSE ? wbuf_s : ring_s + (hw ? ((2 + 2 * half) & 3) : ((1 + 2 * half) & 3)) * DP * 4u;
         const float p0 = *shp<const float>(tg.pp0 + 4u * f0), p1 = *shp<const float>(tg.pp1 + 4u * f1);
         const float w0 = *shp<const float>(wb + 4u * f0), w1 = *shp<const float>(wb + 4u * f1);
