@@ -856,7 +856,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
       const int kk = lane < h ? lane : h - 1;
       const uint2 rky = cs.tn[kk + 1];
       const uint32_t Tk = rky.x, N4k = rky.y;
-      const float* pp = cs.priv + lane * (DP + 1);
+      const float* pp = cs.priv + kk * (DP + 1);   // lanes past h: the last row's copy
       float rbest = INF;
       int rargj = 0x7fffffff;
       if (w == 1) {
@@ -902,7 +902,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
         best += capQ * (float)(k + 1);   // undo the rectangle's per-target shift
         // f and c' of the winner (the rectangle tracked only its j)
         int argf, argc;
-        if (argj == 0) {
+        if (argj == 0 || argj >= h) {    // (argj >= h: a lane past h that found no candidate)
           argf = span_f(Tk, N4k, smem, Dm1);
           argc = kStart;
         } else {
@@ -1044,9 +1044,11 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
       if (has_next) {
         // this lane's target pair t0 = lane & 15, t1 = t0 + 16 of block b+1
         const int t0 = lane & 15, t1 = t0 + 16;
-        const uint2 r0 = cs.tn[min(Kn + t0, h - 1) + 1], r1 = cs.tn[min(Kn + t1, h - 1) + 1];
-        const float* pp0 = cs.priv + t0 * (DP + 1);
-        const float* pp1 = cs.priv + t1 * (DP + 1);
+        // (targets past h duplicate the last row: only built priv rows are read)
+        const int k0 = min(Kn + t0, h - 1), k1 = min(Kn + t1, h - 1);
+        const uint2 r0 = cs.tn[k0 + 1], r1 = cs.tn[k1 + 1];
+        const float* pp0 = cs.priv + (k0 - Kn) * (DP + 1);
+        const float* pp1 = cs.priv + (k1 - Kn) * (DP + 1);
         tg = Tg{(uint32_t)__cvta_generic_to_shared(pp0), (uint32_t)__cvta_generic_to_shared(pp1),
                 r0.x, r1.x, r0.y, r1.y};
         if (w == 1 && hw == 0) {       // j = 0: first stixel spans 0..k (Eq. 5)
