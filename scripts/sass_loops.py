@@ -5,7 +5,7 @@ import re
 import subprocess
 import sys
 
-lib = "paper_1610_04124_b200/libstixels.so"
+lib = sys.argv[3] if len(sys.argv) > 3 else "paper_1610_04124_b200/libstixels.so"
 pat = sys.argv[1] if len(sys.argv) > 1 else "dp_kernelILi128"
 maxlen = int(sys.argv[2]) if len(sys.argv) > 2 else 400
 txt = subprocess.run(["cuobjdump", "-sass", lib], capture_output=True, text=True).stdout
