@@ -690,7 +690,8 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
     }
   };
 
-  float fr[NS];                        // builder warp: W[f][32 bt] for f = lane + 32c
+  constexpr int NB = NS / 2;           // f slices per builder warp (warps 1 and 2)
+  float fr[NB];                        // builder warps: W[f][32 bt] for f = lane + 32 (c0 + c)
 
   bool first_item = true;
   (void)first_item;
@@ -768,15 +769,14 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
     }
     named_bar(bar_col, kCW * 32);
 
-    // build priv W-rows of block bt (rectangle warps, f slices rw, rw+3, ...) and the
-    // anchor row 32(bt+1): a sequential prefix over rows, per f.  The
-    // row offsets come from lane registers by shuffle; loads of 8 rows are issued
-    // before their prefix chain.
-    // One warp (w == 1) builds them: lane l owns f = l + 32c (c < NS), so both the
-    // E' loads and the priv stores are bank-conflict free; loads of 8 rows are
-    // issued before their prefix chain.  (The other rectangle warps wait: a
-    // sequential prefix does not split well, and waiting costs no issue slots.)
+    // build priv W-rows of block bt and the anchor row 32(bt+1): a sequential
+    // prefix over rows, per f, so the f slices are independent.  Two
+    // warps (w = 1, 2) build them, each half of the slices: lane l owns
+    // f = l + 32 (c0 + c), c < NB, so both the E' loads and the priv stores are
+    // bank-conflict free.  The row offsets come from lane registers by shuffle;
+    // loads of 8 rows are issued before their prefix chain.
     auto build_priv = [&](int bt) {
+      const int c0 = (w - 1) * NB;
       const int K0b = bt << 5;
       const int rows = min(32, h - K0b);
       const uint32_t eor = cs.eo[K0b + min(lane, rows - 1)] >> 16;
@@ -785,31 +785,31 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
 #pragma unroll
       for (int i0 = 0; i0 < 32; i0 += 8) {
         if (i0 < rows) {
-          float x[8][NS];
+          float x[8][NB];
 #pragma unroll
           for (int r = 0; r < 8; ++r) {
             const uint32_t e = __shfl_sync(0xffffffffu, eor, i0 + r);
 #pragma unroll
-            for (int c = 0; c < NS; ++c) {
-              if constexpr (PAIR2D) x[r][c] = __ldg(a.E2g + e * DP + 32 * c + lane);
-              else x[r][c] = *shp<const float>(src_s + e + 128u * c);
+            for (int c = 0; c < NB; ++c) {
+              if constexpr (PAIR2D) x[r][c] = __ldg(a.E2g + e * DP + 32 * (c0 + c) + lane);
+              else x[r][c] = *shp<const float>(src_s + e + 128u * (c0 + c));
             }
           }
 #pragma unroll
           for (int r = 0; r < 8; ++r) {
             if (i0 + r < rows) {
 #pragma unroll
-              for (int c = 0; c < NS; c += 2) {
+              for (int c = 0; c < NB; c += 2) {
                 fadd2_inplace(fr[c], fr[c + 1], x[r][c], x[r][c + 1]);
-                *shp<float>(dst_s + ((i0 + r) * (DP + 1) + 32 * c) * 4u) = fr[c];
-                *shp<float>(dst_s + ((i0 + r) * (DP + 1) + 32 * c + 32) * 4u) = fr[c + 1];
+                *shp<float>(dst_s + ((i0 + r) * (DP + 1) + 32 * (c0 + c)) * 4u) = fr[c];
+                *shp<float>(dst_s + ((i0 + r) * (DP + 1) + 32 * (c0 + c) + 32) * 4u) = fr[c + 1];
               }
             }
           }
         }
       }
 #pragma unroll
-      for (int c = 0; c < NS; ++c) ANg[(bt + 1) * DP + 32 * c + lane] = fr[c];
+      for (int c = 0; c < NB; ++c) ANg[(bt + 1) * DP + 32 * (c0 + c) + lane] = fr[c];
     };
     // triangle cells of block bt: bottom K0+1+j', target K0+k' (k' > j'); their
     // bottoms' W-rows are the block's own priv rows: data term (absolute),
@@ -844,9 +844,9 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
       }
     };
 
-    if (w == 1) {
+    if (w == 1 || w == 2) {
 #pragma unroll
-      for (int c = 0; c < NS; ++c) fr[c] = 0.f;
+      for (int c = 0; c < NB; ++c) fr[c] = 0.f;
       build_priv(0);
     }
     named_bar(bar_col, kCW * 32);
@@ -1033,7 +1033,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
         STX_STAMP(b, 1);
         if (has_next) named_bar(bar_x, kCW * 32);   // block b+1's priv rows are ready
       } else if (has_next) {
-        if (w == 1) build_priv(bn);      // block b's priv rows are no longer needed
+        if (w == 1 || w == 2) build_priv(bn);   // block b's priv rows are no longer needed
         if (w == 1) STX_STAMP(b, 2);
         named_bar(bar_rect, 3 * 32);
         asm volatile("bar.arrive %0, %1;" ::"r"(bar_x), "r"(kCW * 32) : "memory");
