@@ -276,8 +276,8 @@ struct ColSmem {
                     //                16-byte record each (one LDS.128 in the serial chain):
                     //                {object data term, the same plus its O-above-G prior
                     //                (gravity level), object mean f (int bits), unused}
-  uint4* rec;       // [h+3][2]       row j: {AO0,AO1,AGm,AGh} {AGl, T[j], N4[j], ordthr | drp<<16}
-  uint2* tn;        // [h+1]          row j: {T[j], N4[j]} (compact copy for per-lane rows)
+  uint4* rec;       // [h+3][2]       row j: {AO0,AO1,AGm,AGh} {T[j], N4[j], AGl, ordthr | drp<<16}
+                    //                ({T, N4} also read per lane as a uint2: tn_at)
   uint32_t* eo;     // [h+2]          lo16: ring window byte offset; hi16: E0 byte offset
   uint16_t* argO;   // [h]            j | c'<<12
   uint16_t* argG;   // [h]            j (pred class O, or start if j == 0)
@@ -320,7 +320,6 @@ __host__ __device__ inline int col_smem_bytes(int h) {
   b += al16(kCW * ring_stride<DP, SPARSE>() * 4);
   b += kTri * 16;
   b += al16((h + 3) * 32);
-  b += al16((h + 1) * 8);
   b += al16((h + 2) * 4);
   b += al16(h * 2) * 3;
   b += al16(h);
@@ -343,7 +342,6 @@ __device__ inline ColSmem carve(uint8_t* p, int h) {
   w.ring = reinterpret_cast<float*>(p); p += al16(kCW * ring_stride<DP, SPARSE>() * 4);
   w.cell = reinterpret_cast<float4*>(p); p += kTri * 16;
   w.rec = reinterpret_cast<uint4*>(p); p += al16((h + 3) * 32);
-  w.tn = reinterpret_cast<uint2*>(p); p += al16((h + 1) * 8);
   w.eo = reinterpret_cast<uint32_t*>(p); p += al16((h + 2) * 4);
   w.argO = reinterpret_cast<uint16_t*>(p); p += al16(h * 2);
   w.argG = reinterpret_cast<uint16_t*>(p); p += al16(h * 2);
@@ -417,8 +415,9 @@ __device__ __forceinline__ RowU unpack_row(uint4 x, uint4 y) {
   RowU u;
   u.AO0 = __uint_as_float(x.x); u.AO1 = __uint_as_float(x.y);
   u.AGm = __uint_as_float(x.z); u.AGh = __uint_as_float(x.w);
-  u.AGl = __uint_as_float(y.x);
-  u.T = y.y; u.N4 = y.z; u.ordthr = (int)(y.w & 0xffffu); u.drp = (int)(y.w >> 16);
+  u.T = y.x; u.N4 = y.y;
+  u.AGl = __uint_as_float(y.z);
+  u.ordthr = (int)(y.w & 0xffffu); u.drp = (int)(y.w >> 16);
   return u;
 }
 __device__ __forceinline__ RowU load_row(const uint4* rec, int j) {
@@ -515,6 +514,8 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
   const uint8_t* Eb = reinterpret_cast<const uint8_t*>(E);
 
   ColSmem cs = carve<DP, SPARSE>(smem + a.shared_bytes + cslot * a.col_bytes, h);
+  // {T[j], N4[j]} of row j: the first 8 bytes of the record's second half
+  auto tn_at = [&](int j) { return *reinterpret_cast<const uint2*>(cs.rec + 2 * j + 1); };
   float* ringw = cs.ring + w * ring_stride<DP, SPARSE>();
   const float INF = __int_as_float(0x7f800000);
   const int slot_global = blockIdx.x * a.cols_per_cta + cslot;
@@ -726,7 +727,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
       if (v < 2) {                       // padding rows h+1, h+2 and row 0: T = N4 = 0
         cs.rec[2 * (h + 1 + v) + 1] = make_uint4(0, 0, 0, (uint32_t)kNoBand << 16);
         cs.rec[2 * (h + 1 + v)] = make_uint4(0, 0, 0, 0);
-        if (v == 0) { cs.rec[1].y = 0; cs.rec[1].z = 0; cs.tn[0] = make_uint2(0, 0); }
+        if (v == 0) { cs.rec[1].x = 0; cs.rec[1].y = 0; }
       }
       // E offsets of this row
       int dmr = valid ? a.D - dr : a.dmr_inv;
@@ -759,8 +760,8 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
           const uint32_t x = (w == 2) ? t : (t ? 4u : 0u);
           const uint32_t in = warp_incl_scan(x, lane) + cu;
           if (v < h) {
-            if (w == 2) { cs.rec[2 * (v + 1) + 1].y = in; cs.tn[v + 1].x = in; }   // T[v+1]
-            else { cs.rec[2 * (v + 1) + 1].z = in; cs.tn[v + 1].y = in; }         // N4[v+1]
+            if (w == 2) cs.rec[2 * (v + 1) + 1].x = in;   // T[v+1]
+            else cs.rec[2 * (v + 1) + 1].y = in;          // N4[v+1]
           }
           cu = __shfl_sync(0xffffffffu, in, 31);
         }
@@ -824,8 +825,8 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
         const int jp = jk & 0xff, kp = jk >> 8;
         const int k = K0b + kp;
         if (k < h) {
-          const uint2 ry = cs.tn[K0b + jp + 1];
-          const uint2 rk = cs.tn[k + 1];
+          const uint2 ry = tn_at(K0b + jp + 1);
+          const uint2 rk = tn_at(k + 1);
           int f = span_f(rk.x - ry.x, rk.y - ry.y, smem, Dm1);
           float data = (cs.priv[kp * (DP + 1) + f] - cs.priv[jp * (DP + 1) + f]) + capQ * (float)(kp - jp);
           const int jr = K0b + jp + 1;
@@ -854,7 +855,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
     // block 0 has only the j = 0 candidate (Eq. 5) and its triangle
     {
       const int kk = lane < h ? lane : h - 1;
-      const uint2 rky = cs.tn[kk + 1];
+      const uint2 rky = tn_at(kk + 1);
       const uint32_t Tk = rky.x, N4k = rky.y;
       const float* pp = cs.priv + kk * (DP + 1);   // lanes past h: the last row's copy
       float rbest = INF;
@@ -887,7 +888,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
       if (w == 0) {
         // ============ serial warp: block b's triangle and finalisation ============
         const int kk = k < h ? k : h - 1;
-        const uint2 rky = cs.tn[kk + 1];
+        const uint2 rky = tn_at(kk + 1);
         const uint32_t N4k = rky.y;
         const uint32_t Tk = rky.x;
         const float pg0 = PGg[kk], pg1 = PGg[kk + 1], ps0 = PSg[kk], ps1 = PSg[kk + 1];
@@ -1023,7 +1024,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
           cs.rec[2 * (k + 1)] = make_uint4(__float_as_uint((best + a.kOO_lo) - sh), __float_as_uint((best + a.kOO_hi) - sh),
                                            __float_as_uint((CGk + a.kGO_mid) - sh), __float_as_uint((CGk + a.kGO_hi) - sh));
           uint32_t* ry = reinterpret_cast<uint32_t*>(cs.rec + 2 * (k + 1) + 1);
-          ry[0] = __float_as_uint((CGk + a.kGO_lo) - sh);
+          ry[2] = __float_as_uint((CGk + a.kGO_lo) - sh);
           reinterpret_cast<uint16_t*>(ry + 3)[0] = (uint16_t)(argf + a.ord_margin);   // ordthr (drp kept)
           cs.argO[k] = (uint16_t)(argj | (argc << 12));
           cs.argG[k] = (uint16_t)aG;
@@ -1046,7 +1047,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
         const int t0 = lane & 15, t1 = t0 + 16;
         // (targets past h duplicate the last row: only built priv rows are read)
         const int k0 = min(Kn + t0, h - 1), k1 = min(Kn + t1, h - 1);
-        const uint2 r0 = cs.tn[k0 + 1], r1 = cs.tn[k1 + 1];
+        const uint2 r0 = tn_at(k0 + 1), r1 = tn_at(k1 + 1);
         const float* pp0 = cs.priv + (k0 - Kn) * (DP + 1);
         const float* pp1 = cs.priv + (k1 - Kn) * (DP + 1);
         tg = Tg{(uint32_t)__cvta_generic_to_shared(pp0), (uint32_t)__cvta_generic_to_shared(pp1),
