@@ -820,14 +820,18 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
       const int K0b = bt << 5;
       const int jn = min(K0b + 31, h - 1) - K0b;
       const int ncell = tri_off(jn);
-      for (int idx = t0; idx < ncell; idx += nthr) {
-        const uint32_t jk = tri_jk[idx];
+      // {T, N4} of the block's rows K0b+1+l in lane l: the cells' row reads become
+      // shuffles (the records' 32-byte stride would make them 8-way bank conflicts)
+      const uint2 tnl = tn_at(min(K0b + lane + 1, h));
+      for (int base = t0 - lane; base < ncell; base += nthr) {   // warp-uniform trip count
+        const int idx = base + lane;
+        const uint32_t jk = tri_jk[min(idx, kTri - 1)];
         const int jp = jk & 0xff, kp = jk >> 8;
         const int k = K0b + kp;
-        if (k < h) {
-          const uint2 ry = tn_at(K0b + jp + 1);
-          const uint2 rk = tn_at(k + 1);
-          int f = span_f(rk.x - ry.x, rk.y - ry.y, smem, Dm1);
+        const uint32_t ryx = __shfl_sync(0xffffffffu, tnl.x, jp), ryy = __shfl_sync(0xffffffffu, tnl.y, jp);
+        const uint32_t rkx = __shfl_sync(0xffffffffu, tnl.x, kp), rky = __shfl_sync(0xffffffffu, tnl.y, kp);
+        if (idx < ncell && k < h) {
+          int f = span_f(rkx - ryx, rky - ryy, smem, Dm1);
           float data = (cs.priv[kp * (DP + 1) + f] - cs.priv[jp * (DP + 1) + f]) + capQ * (float)(kp - jp);
           const int jr = K0b + jp + 1;
           const int2 th = thrS[jr];
