@@ -485,7 +485,7 @@ def main():
                "h2d_bytes_per_step": eb * H_IMG * pitch,
                "d2h_bytes_per_step": eb * hd2.n_cols * (hd2.cap * 12 + 8),
                "frames_per_step": eb, "max_stixels": 128,
-               "note": "stixels_compute_host: pinned host buffers, 32-frame chunks on 2 "
+               "note": "stixels_compute_host: pinned host buffers, ~32-frame stages (29 at 1024x440) on 2 "
                        "streams, synchronous call; wall clock max over ranks"}
         hd2.destroy()
 

@@ -610,7 +610,19 @@ int stixels_compute_host(stixels_handle* h, const void* h_disp, int64_t pitch, i
   if (!h_disp || !h_out || !h_count || batch < 1 || pitch < (int64_t)h->W * bpp)
     return fail(h, STIXELS_ERR_ARG, "bad host pointer, batch or pitch");
   cudaSetDevice(h->device);
-  const int chunk = std::min(h->max_batch, 32);   // frames per H2D / compute / D2H stage
+  // frames per H2D / compute / D2H stage: about 32, chosen so that the stage's
+  // columns fill the column slots evenly (1024x440: 29 frames = 5916 columns =
+  // 10 per slot on 588 of 592 slots; 32 frames would leave 16 slots a 12th column)
+  int chunk = std::min(h->max_batch, 32);
+  {
+    const long slots = (long)h->grid * h->cols_per_cta;
+    double best = -1.0;
+    for (int f = std::min(h->max_batch, 40); f >= std::min(h->max_batch, 24); --f) {
+      const long items = (long)f * h->n_cols;
+      const double eff = (double)items / (double)(slots * ((items + slots - 1) / slots));
+      if (eff > best + 1e-3) { best = eff; chunk = f; }
+    }
+  }
   const size_t in_b = (size_t)h->H * pitch;
   if (h->h_chunk != chunk || h->h_pitch != pitch) {
     for (int i = 0; i < 2; ++i) {
