@@ -27,6 +27,7 @@ struct stixels_handle {
   int n_cols = 0, cap = 0, dp_slots = 128, cols_per_cta = 0, smem = 0, grid = 0, sms = 0;
   bool sparse = true;
   bool pair2d = false;          // NEXT f2: sigma_O(f) table given
+  bool iw = false;              // int32 W-rows with atomic band rounds (band <= 3, exact mode)
   int red_tc = 0, red_smem = 0, red_w2 = 0;
   DPArgs args{};
   float* d_E = nullptr;
@@ -344,6 +345,7 @@ int stixels_create(const stixels_params* params, int width, int height, int max_
       }
   }
   const bool sparse = band <= 7;
+  const bool iw = sparse && !pair2d && band <= 3 && params->cost_frac_bits > 0;
   // magic reciprocals: floor(y/(2n)) = umulhi(y, ceil(2^31/n))
   std::vector<uint32_t> M2(height + 1);
   M2[0] = 0;
@@ -410,6 +412,7 @@ int stixels_create(const stixels_params* params, int width, int height, int max_
   }
   h->sparse = sparse;
   h->pair2d = pair2d;
+  h->iw = iw;
   A.h = height; A.D = D; A.n_cols = h->n_cols; A.cap = h->cap;
   A.LG = LGr; A.gG_stride = sig_g.empty() ? 0 : LGr; A.LS = (int)gS.size(); A.esz = esz; A.dmr_inv = einv;
   A.ord_margin = params->ord_margin;
@@ -428,9 +431,11 @@ int stixels_create(const stixels_params* params, int width, int height, int max_
   auto kfun = [&]() -> const void* {
     if (DPv == 128)
       return pair2d ? (const void*)dp_kernel<128, true, true>
-                    : sparse ? (const void*)dp_kernel<128, true, false> : (const void*)dp_kernel<128, false, false>;
+             : iw   ? (const void*)dp_kernel<128, true, false, true>
+             : sparse ? (const void*)dp_kernel<128, true, false> : (const void*)dp_kernel<128, false, false>;
     return pair2d ? (const void*)dp_kernel<256, true, true>
-                  : sparse ? (const void*)dp_kernel<256, true, false> : (const void*)dp_kernel<256, false, false>;
+           : iw   ? (const void*)dp_kernel<256, true, false, true>
+           : sparse ? (const void*)dp_kernel<256, true, false> : (const void*)dp_kernel<256, false, false>;
   };
   int cb = DPv == 128 ? (sparse ? col_smem_bytes<128, true>(height) : col_smem_bytes<128, false>(height))
                       : (sparse ? col_smem_bytes<256, true>(height) : col_smem_bytes<256, false>(height));
@@ -549,10 +554,12 @@ static int launch_dp(stixels_handle* h, const uint16_t* d_cols, int batch, stixe
   const int threads = C * kCW * 32;
   if (h->dp_slots == 128) {
     if (h->pair2d) dp_kernel<128, true, true><<<grid, threads, smem, s>>>(A);
+    else if (h->iw) dp_kernel<128, true, false, true><<<grid, threads, smem, s>>>(A);
     else if (h->sparse) dp_kernel<128, true, false><<<grid, threads, smem, s>>>(A);
     else dp_kernel<128, false, false><<<grid, threads, smem, s>>>(A);
   } else {
     if (h->pair2d) dp_kernel<256, true, true><<<grid, threads, smem, s>>>(A);
+    else if (h->iw) dp_kernel<256, true, false, true><<<grid, threads, smem, s>>>(A);
     else if (h->sparse) dp_kernel<256, true, false><<<grid, threads, smem, s>>>(A);
     else dp_kernel<256, false, false><<<grid, threads, smem, s>>>(A);
   }

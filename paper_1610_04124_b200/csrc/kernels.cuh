@@ -462,7 +462,12 @@ __device__ __forceinline__ void fadd2_inplace(float& a0, float& a1, float b0, fl
 template <int DP>
 __host__ __device__ constexpr int wt_rows() { return DP + 17; }   // drp 0 .. no_band()
 
-template <int DP, bool SPARSE, bool PAIR2D>
+// IW (sparse, band <= 3, exact mode only): the rectangle's W-row buffers hold int32
+// quanta, and the four pixel updates of a bottom pair are one round of native
+// shared-memory integer atomics on 8-lane groups (float atomics would be CAS
+// loops).  Exact: every W entry is an integer number of quanta below 2^24 (L#22),
+// so the order of the adds does not matter and the gathers convert exactly.
+template <int DP, bool SPARSE, bool PAIR2D, bool IW = false>
 __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_constant__ DPArgs a) {
   constexpr int NR = DP / 128;         // LDS.128 ring windows per lane
   constexpr int NS = DP / 32;          // 32-wide f slices
@@ -577,6 +582,14 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
   const uint32_t bbuf2_s = ring_s + ((lane < 16) ? 0u : ring_b1<DP, SPARSE>()) + (uint32_t)((boff - 1) * 4);
   // the W-row this half reads: buffer 1 holds W_jA (half 0), buffer 0 W_{jA+1} (half 1)
   const uint32_t wbuf_s = ring_s + ((lane < 16) ? ring_b1<DP, SPARSE>() : 0u);
+  // IW atomic round: 8-lane group g = lane >> 3 applies one pixel at offset
+  // (lane & 7) - 3: g0 pixel jA -> buffer 1, g1 pixel jA+2 -> buffer 0 (half 0's
+  // rows), g2 pixel jA+1 -> buffer 1, g3 pixel jA+1 -> buffer 0 (half 1's row).
+  // Lane 7 of a group (offset +4) adds 0 (band <= 3) inside the guard entries, so
+  // the round needs no predicate.
+  const int igrp = lane >> 3;
+  const uint32_t ibase_s = ring_s + ((igrp & 1) ? 0u : ring_b1<DP, SPARSE>()) + (uint32_t)(((lane & 7) - 4) * 4);
+  const int iwt = (int)a.wt[(lane & 7) + 4];   // cap - Pair at offset (lane & 7) - 3
   auto rect_run = [&](float (&rr)[4 * NR], int j0, int nsteps, const Tg& tg, Acc& acc) {
     // sparse band round: f = drp - 1 + boff always lands in the buffer or its
     // guards (no range test; zero-weight lanes write back their value)
@@ -604,8 +617,23 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
       const uint32_t M = *shp<const uint32_t>(m2_s + n4);
       return (int)__umulhi((Tk - r.T) >> (kRBits - 1), M);   // < D: inputs below D - 1/2 (L#27)
     };
+    auto band_i = [&](int drp) {
+      atomicAdd(shp<int>(ibase_s + 4u * (uint32_t)drp), -iwt);
+    };
     RowU r = rowj(j0 + hw);
-    if constexpr (SPARSE) {
+    if constexpr (SPARSE && IW) {
+      // both buffers := W_{j0-1} (int32); then buffer 1 = W_{j0}, buffer 0 = W_{j0+1}
+      const int drm = rowj(j0 - 1).drp;
+#pragma unroll
+      for (int q = 0; q < NR; ++q) {
+        const int4 v = make_int4(__float2int_rn(rr[4 * q]), __float2int_rn(rr[4 * q + 1]),
+                                 __float2int_rn(rr[4 * q + 2]), __float2int_rn(rr[4 * q + 3]));
+        *shp<int4>(ring_s + 16u * lane + 512u * q) = v;
+        *shp<int4>(ring_s + ring_b1<DP, SPARSE>() + 16u * lane + 512u * q) = v;
+      }
+      __syncwarp();
+      band_i(igrp == 1 ? r.drp : (igrp == 2 ? kNoBand : drm));   // g0, g3: pixel j0-1; g1: j0
+    } else if constexpr (SPARSE) {
       // both buffers := W_{j0-1}; then buffer 1 = W_{j0}, buffer 0 = W_{j0+1}
       const int drm = rowj(j0 - 1).drp;
 #pragma unroll
@@ -639,10 +667,20 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
         const int thA = th.x, thB = th.y;
         const uint32_t wb = SPARSE ? wbuf_s : ring_s + (hw ? ((2 + 2 * half) & 3) : ((1 + 2 * half) & 3)) * DP * 4u;
         const float p0 = *shp<const float>(tg.pp0 + 4u * f0), p1 = *shp<const float>(tg.pp1 + 4u * f1);
-        const float w0 = *shp<const float>(wb + 4u * f0), w1 = *shp<const float>(wb + 4u * f1);
+        float w0, w1;
+        if constexpr (IW) {
+          w0 = (float)*shp<const int>(wb + 4u * f0);
+          w1 = (float)*shp<const int>(wb + 4u * f1);
+        } else {
+          w0 = *shp<const float>(wb + 4u * f0);
+          w1 = *shp<const float>(wb + 4u * f1);
+        }
         cell(r, jm, thA, thB, f0, p0 - w0, acc.b0, acc.a0);
         cell(r, jm, thA, thB, f1, p1 - w1, acc.b1, acc.a1);
-        if constexpr (SPARSE) {
+        if constexpr (SPARSE && IW) {
+          __syncwarp();
+          band_i(igrp == 1 ? n.drp : r.drp);       // W_jA -> W_{jA+2}, W_{jA+1} -> W_{jA+3}
+        } else if constexpr (SPARSE) {
           // buffer 1: W_jA -> W_{jA+2} (pixels jA: half 0, jA+1: half 1);
           // buffer 0: W_{jA+1} -> W_{jA+3} (pixels jA+1: half 1, jA+2: half 0's next row)
           __syncwarp();
