@@ -504,7 +504,11 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
   float* E = reinterpret_cast<float*>(smem + kM2Pad + al16((h + 1) * 4));
   uint16_t* tri_jk = reinterpret_cast<uint16_t*>(smem + kM2Pad + al16((h + 1) * 4) + e_copies<SPARSE>() * a.esz * 4);
   for (int i = threadIdx.x; i <= h; i += blockDim.x) M2s[i] = a.M2[i];
-  for (int i = threadIdx.x; i < e_copies<SPARSE>() * a.esz; i += blockDim.x) E[i] = a.E[i];
+  // IW: the object pair-cost window in int32 quanta (exact-mode costs are integers)
+  for (int i = threadIdx.x; i < e_copies<SPARSE>() * a.esz; i += blockDim.x) {
+    if constexpr (IW) reinterpret_cast<int*>(E)[i] = __float2int_rn(a.E[i]);
+    else E[i] = a.E[i];
+  }
   float* WT = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(tri_jk) + al16(kTri * 2));
   if constexpr (PAIR2D)
     for (int i = threadIdx.x; i < wt_rows<DP>() * 16; i += blockDim.x) WT[i] = a.WTg[i];
@@ -571,7 +575,12 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
   // before the current pair's table loads.  Shared memory is addressed with
   // explicit 32-bit offsets.
   struct Tg { uint32_t pp0, pp1, T0, T1, N0, N1; };   // priv rows, T[k+1], N4[k+1] of t0 / t1
-  struct Acc { float b0, b1; int a0, a1; };           // running minima {cost, argj} of t0 / t1
+  // Cost type of the rectangle: IW keeps priv rows, W-rows, records and the running
+  // minima in int32 quanta (exact mode), so a cell is p - w + min(aO, aG) in one
+  // IADD3 and no conversion; otherwise fp32.
+  using CT = std::conditional_t<IW, int, float>;
+  constexpr int kRectUnroll = IW ? 2 : 1;
+  struct Acc { CT b0, b1; int a0, a1; };              // running minima {cost, argj} of t0 / t1
   const int hw = lane >> 4;
   const uint32_t rec_s = (uint32_t)__cvta_generic_to_shared(cs.rec);
   const uint32_t m2_s = (uint32_t)__cvta_generic_to_shared(M2s);   // (dynamic smem does not start at 0)
@@ -606,11 +615,19 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
       const uint4* q = shp<const uint4>(rec_s + 32u * (uint32_t)j);
       return unpack_row(q[0], q[1]);
     };
-    auto cell = [&](const RowU& r, int j, int thA, int thB, int f, float pw, float& best, int& argj) {
-      float aO = (f > r.ordthr) ? r.AO1 : r.AO0;
-      float aG = (f >= thA) ? r.AGh : ((f < thB) ? r.AGl : r.AGm);
-      float cand = pw + fminf(aO, aG);
-      if (cand < best) { best = cand; argj = j; }
+    auto cell = [&](const RowU& r, int j, int thA, int thB, int f, CT p, CT w, CT& best, int& argj) {
+      if constexpr (IW) {              // records hold int32 quanta (bits in the float fields)
+        const int aO = (f > r.ordthr) ? __float_as_int(r.AO1) : __float_as_int(r.AO0);
+        const int aG = (f >= thA) ? __float_as_int(r.AGh)
+                                  : ((f < thB) ? __float_as_int(r.AGl) : __float_as_int(r.AGm));
+        const int cand = p - w + min(aO, aG);
+        if (cand < best) { best = cand; argj = j; }
+      } else {
+        float aO = (f > r.ordthr) ? r.AO1 : r.AO0;
+        float aG = (f >= thA) ? r.AGh : ((f < thB) ? r.AGl : r.AGm);
+        float cand = (p - w) + fminf(aO, aG);
+        if (cand < best) { best = cand; argj = j; }
+      }
     };
     auto fmean = [&](const RowU& r, uint32_t Tk, uint32_t N4k) {
       const uint32_t n4 = N4k - r.N4;
@@ -626,8 +643,8 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
       const int drm = rowj(j0 - 1).drp;
 #pragma unroll
       for (int q = 0; q < NR; ++q) {
-        const int4 v = make_int4(__float2int_rn(rr[4 * q]), __float2int_rn(rr[4 * q + 1]),
-                                 __float2int_rn(rr[4 * q + 2]), __float2int_rn(rr[4 * q + 3]));
+        const int4 v = make_int4(__float_as_int(rr[4 * q]), __float_as_int(rr[4 * q + 1]),   // int32 bits
+                                 __float_as_int(rr[4 * q + 2]), __float_as_int(rr[4 * q + 3]));
         *shp<int4>(ring_s + 16u * lane + 512u * q) = v;
         *shp<int4>(ring_s + ring_b1<DP, SPARSE>() + 16u * lane + 512u * q) = v;
       }
@@ -652,7 +669,9 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
     }
     int f0 = fmean(r, tg.T0, tg.N0), f1 = fmean(r, tg.T1, tg.N1);
     __syncwarp();
-#pragma unroll 1          // 4 bottoms per iteration (A/B with lane pairs: unroll 2 -3.5%, 4 +-0, 8 -13%)
+    // bottoms per iteration (A/B on the B200): fp32 path 4 (unroll 2: -3.5%, 8: -13%);
+    // IW int32 path 8 (unroll 1: -3.7%, 4: +-0)
+#pragma unroll kRectUnroll
     for (int jj = 0; jj < nsteps; jj += 4) {
 #pragma unroll
       for (int half = 0; half < 2; ++half) {
@@ -666,17 +685,10 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
         const int2 th = *shp<const int2>(thr_s + 8u * (uint32_t)jm);
         const int thA = th.x, thB = th.y;
         const uint32_t wb = SPARSE ? wbuf_s : ring_s + (hw ? ((2 + 2 * half) & 3) : ((1 + 2 * half) & 3)) * DP * 4u;
-        const float p0 = *shp<const float>(tg.pp0 + 4u * f0), p1 = *shp<const float>(tg.pp1 + 4u * f1);
-        float w0, w1;
-        if constexpr (IW) {
-          w0 = (float)*shp<const int>(wb + 4u * f0);
-          w1 = (float)*shp<const int>(wb + 4u * f1);
-        } else {
-          w0 = *shp<const float>(wb + 4u * f0);
-          w1 = *shp<const float>(wb + 4u * f1);
-        }
-        cell(r, jm, thA, thB, f0, p0 - w0, acc.b0, acc.a0);
-        cell(r, jm, thA, thB, f1, p1 - w1, acc.b1, acc.a1);
+        const CT p0 = *shp<const CT>(tg.pp0 + 4u * f0), p1 = *shp<const CT>(tg.pp1 + 4u * f1);
+        const CT w0 = *shp<const CT>(wb + 4u * f0), w1 = *shp<const CT>(wb + 4u * f1);
+        cell(r, jm, thA, thB, f0, p0, w0, acc.b0, acc.a0);
+        cell(r, jm, thA, thB, f1, p1, w1, acc.b1, acc.a1);
         if constexpr (SPARSE && IW) {
           __syncwarp();
           band_i(igrp == 1 ? n.drp : r.drp);       // W_jA -> W_{jA+2}, W_{jA+1} -> W_{jA+3}
@@ -699,13 +711,17 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
   // The step's result of target lane (t = lane): the two halves' minima merged,
   // ties to the lower bottom (the first in bottom order, L#17).
   auto merge_part = [&](const Acc& acc) {
-    const float sb = __shfl_xor_sync(0xffffffffu, hw ? acc.b0 : acc.b1, 16);
+    const CT sb = __shfl_xor_sync(0xffffffffu, hw ? acc.b0 : acc.b1, 16);
     const int sa = __shfl_xor_sync(0xffffffffu, hw ? acc.a0 : acc.a1, 16);
-    float mb = hw ? acc.b1 : acc.b0;
+    CT mb = hw ? acc.b1 : acc.b0;
     int ma = hw ? acc.a1 : acc.a0;
     if (sb < mb || (sb == mb && sa < ma)) { mb = sb; ma = sa; }
-    return make_float2(mb, __int_as_float(ma));
+    float mf;
+    if constexpr (IW) mf = (mb == 0x7fffffff) ? INF : (float)mb;   // exact: |mb| < 2^24
+    else mf = mb;
+    return make_float2(mf, __int_as_float(ma));
   };
+
   // Full 32-row chunks m < mend for this warp's targets, handed out dynamically;
   // the anchor row of the next chunk is prefetched from L2 while one runs.
   auto bulk_chunks = [&](int mend, const Tg& tg, Acc& acc) {
@@ -730,7 +746,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
   };
 
   constexpr int NB = NS / 2;           // f slices per builder warp (warps 1 and 2)
-  float fr[NB];                        // builder warps: W[f][32 bt] for f = lane + 32 (c0 + c)
+  CT fr[NB];                           // builder warps: W[f][32 bt] for f = lane + 32 (c0 + c)
 
   bool first_item = true;
   (void)first_item;
@@ -824,14 +840,14 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
 #pragma unroll
       for (int i0 = 0; i0 < 32; i0 += 8) {
         if (i0 < rows) {
-          float x[8][NB];
+          CT x[8][NB];
 #pragma unroll
           for (int r = 0; r < 8; ++r) {
             const uint32_t e = __shfl_sync(0xffffffffu, eor, i0 + r);
 #pragma unroll
             for (int c = 0; c < NB; ++c) {
               if constexpr (PAIR2D) x[r][c] = __ldg(a.E2g + e * DP + 32 * (c0 + c) + lane);
-              else x[r][c] = *shp<const float>(src_s + e + 128u * (c0 + c));
+              else x[r][c] = *shp<const CT>(src_s + e + 128u * (c0 + c));
             }
           }
 #pragma unroll
@@ -839,16 +855,21 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
             if (i0 + r < rows) {
 #pragma unroll
               for (int c = 0; c < NB; c += 2) {
-                fadd2_inplace(fr[c], fr[c + 1], x[r][c], x[r][c + 1]);
-                *shp<float>(dst_s + ((i0 + r) * (DP + 1) + 32 * (c0 + c)) * 4u) = fr[c];
-                *shp<float>(dst_s + ((i0 + r) * (DP + 1) + 32 * (c0 + c) + 32) * 4u) = fr[c + 1];
+                if constexpr (IW) {
+                  fr[c] += x[r][c];
+                  fr[c + 1] += x[r][c + 1];
+                } else {
+                  fadd2_inplace(fr[c], fr[c + 1], x[r][c], x[r][c + 1]);
+                }
+                *shp<CT>(dst_s + ((i0 + r) * (DP + 1) + 32 * (c0 + c)) * 4u) = fr[c];
+                *shp<CT>(dst_s + ((i0 + r) * (DP + 1) + 32 * (c0 + c) + 32) * 4u) = fr[c + 1];
               }
             }
           }
         }
       }
 #pragma unroll
-      for (int c = 0; c < NB; ++c) ANg[(bt + 1) * DP + 32 * (c0 + c) + lane] = fr[c];
+      for (int c = 0; c < NB; ++c) reinterpret_cast<CT*>(ANg)[(bt + 1) * DP + 32 * (c0 + c) + lane] = fr[c];
     };
     // triangle cells of block bt: bottom K0+1+j', target K0+k' (k' > j'); their
     // bottoms' W-rows are the block's own priv rows: data term (absolute),
@@ -870,7 +891,8 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
         const uint32_t rkx = __shfl_sync(0xffffffffu, tnl.x, kp), rky = __shfl_sync(0xffffffffu, tnl.y, kp);
         if (idx < ncell && k < h) {
           int f = span_f(rkx - ryx, rky - ryy, smem, Dm1);
-          float data = (cs.priv[kp * (DP + 1) + f] - cs.priv[jp * (DP + 1) + f]) + capQ * (float)(kp - jp);
+          const CT* pv = reinterpret_cast<const CT*>(cs.priv);
+          float data = (float)(pv[kp * (DP + 1) + f] - pv[jp * (DP + 1) + f]) + capQ * (float)(kp - jp);
           const int jr = K0b + jp + 1;
           const int2 th = thrS[jr];
           const float pen = (f >= th.x) ? a.kGO_hi : ((f < th.y) ? a.kGO_lo : a.kGO_mid);
@@ -889,7 +911,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
 
     if (w == 1 || w == 2) {
 #pragma unroll
-      for (int c = 0; c < NB; ++c) fr[c] = 0.f;
+      for (int c = 0; c < NB; ++c) fr[c] = 0;
       build_priv(0);
     }
     named_bar(bar_col, kCW * 32);
@@ -904,7 +926,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
       int rargj = 0x7fffffff;
       if (w == 1) {
         int f = span_f(Tk, N4k, smem, Dm1);
-        rbest = pp[f] + a.piFirstO;      // shifted by -cap*(k+1)
+        rbest = (float)reinterpret_cast<const CT*>(pp)[f] + a.piFirstO;   // shifted by -cap*(k+1)
         rargj = 0;
       }
       cs.part[w * 32 + lane] = make_float2(rbest, __int_as_float(rargj));
@@ -954,7 +976,8 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
           const uint32_t th = __ldg(a.thrg + argj);
           float aO = (argf > r.ordthr) ? r.AO1 : r.AO0;
           float aG = (argf >= (int)(th & 0xffffu)) ? r.AGh : ((argf < (int)(th >> 16)) ? r.AGl : r.AGm);
-          argc = (aG <= aO) ? 0 : 1;
+          if constexpr (IW) argc = (__float_as_int(aG) <= __float_as_int(aO)) ? 0 : 1;   // int32 records
+          else argc = (aG <= aO) ? 0 : 1;
         }
         const float kOG = a.kOG;
         // per row j = K0 + lane: {kOG - PG[j], PG[j+1]} for the in-loop ground chain
@@ -1063,10 +1086,11 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
         // shifted by -cap*(k+1)) and the index table
         if (k < h) {
           const float sh = capQ * (float)(k + 1);
-          cs.rec[2 * (k + 1)] = make_uint4(__float_as_uint((best + a.kOO_lo) - sh), __float_as_uint((best + a.kOO_hi) - sh),
-                                           __float_as_uint((CGk + a.kGO_mid) - sh), __float_as_uint((CGk + a.kGO_hi) - sh));
+          auto rb = [](float x) { return IW ? (uint32_t)__float2int_rn(x) : __float_as_uint(x); };   // IW: int32 quanta
+          cs.rec[2 * (k + 1)] = make_uint4(rb((best + a.kOO_lo) - sh), rb((best + a.kOO_hi) - sh),
+                                           rb((CGk + a.kGO_mid) - sh), rb((CGk + a.kGO_hi) - sh));
           uint32_t* ry = reinterpret_cast<uint32_t*>(cs.rec + 2 * (k + 1) + 1);
-          ry[2] = __float_as_uint((CGk + a.kGO_lo) - sh);
+          ry[2] = rb((CGk + a.kGO_lo) - sh);
           reinterpret_cast<uint16_t*>(ry + 3)[0] = (uint16_t)(argf + a.ord_margin);   // ordthr (drp kept)
           cs.argO[k] = (uint16_t)(argj | (argc << 12));
           cs.argG[k] = (uint16_t)aG;
@@ -1082,7 +1106,9 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
         asm volatile("bar.arrive %0, %1;" ::"r"(bar_x), "r"(kCW * 32) : "memory");
       }
       // ======== all warps: block b+1, bottoms final before block b ===============
-      Acc acc{INF, INF, 0x7fffffff, 0x7fffffff};
+      Acc acc;
+      if constexpr (IW) acc = Acc{0x7fffffff, 0x7fffffff, 0x7fffffff, 0x7fffffff};
+      else acc = Acc{INF, INF, 0x7fffffff, 0x7fffffff};
       Tg tg{};
       if (has_next) {
         // this lane's target pair t0 = lane & 15, t1 = t0 + 16 of block b+1
@@ -1095,8 +1121,9 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
         tg = Tg{(uint32_t)__cvta_generic_to_shared(pp0), (uint32_t)__cvta_generic_to_shared(pp1),
                 r0.x, r1.x, r0.y, r1.y};
         if (w == 1 && hw == 0) {       // j = 0: first stixel spans 0..k (Eq. 5)
-          acc.b0 = pp0[span_f(r0.x, r0.y, smem, Dm1)] + a.piFirstO;
-          acc.b1 = pp1[span_f(r1.x, r1.y, smem, Dm1)] + a.piFirstO;
+          const CT pf = IW ? (CT)__float2int_rn(a.piFirstO) : (CT)a.piFirstO;
+          acc.b0 = reinterpret_cast<const CT*>(pp0)[span_f(r0.x, r0.y, smem, Dm1)] + pf;
+          acc.b1 = reinterpret_cast<const CT*>(pp1)[span_f(r1.x, r1.y, smem, Dm1)] + pf;
           acc.a0 = acc.a1 = 0;
         }
         // full chunks m <= b-1: their records (rows <= 32 b) were final before block b
