@@ -214,6 +214,17 @@ __global__ void __launch_bounds__(kRedThreads) reduce_kernel(ReduceArgs a) {
 // adds/mins are exact and every decision matches the oracle.
 // ---------------------------------------------------------------------------
 constexpr int kCW = 4;                 // warps per column
+// IW scale: priv rows, W-rows and the records' predecessor terms are int32 quanta
+// x 32, and each record carries (j - 1) & 31 of its row in the low 5 bits.  A
+// candidate p - w + min(aO, aG) is then (cost x 32) | offset of its bottom in the
+// 32-row block, so one IMNMX keeps the run's minimum and its first bottom; the
+// argmin is decoded once per run.  |cost| < 2^25 (the host's 2^24 check), so the
+// scaled values stay below 2^30.
+constexpr int kIWS = 32;
+// A record term at or beyond 2^24 quanta (an INF prior: a forbidden transition)
+// is stored as 2^30: p - w <= 0 keeps every candidate built on it below 2^30 (no
+// overflow) and above any finite cost; unscaled costs >= 2^24 read back as INF.
+constexpr int kIWBig = 1 << 30;
 
 // Diagnostic phase timeline (build with -DSTX_TRACE; scripts/trace_phases.py):
 // CTA 0's column groups record %globaltimer stamps (ns; one clock for all SM
@@ -506,7 +517,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
   for (int i = threadIdx.x; i <= h; i += blockDim.x) M2s[i] = a.M2[i];
   // IW: the object pair-cost window in int32 quanta (exact-mode costs are integers)
   for (int i = threadIdx.x; i < e_copies<SPARSE>() * a.esz; i += blockDim.x) {
-    if constexpr (IW) reinterpret_cast<int*>(E)[i] = __float2int_rn(a.E[i]);
+    if constexpr (IW) reinterpret_cast<int*>(E)[i] = __float2int_rn(a.E[i]) * kIWS;
     else E[i] = a.E[i];
   }
   float* WT = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(tri_jk) + al16(kTri * 2));
@@ -579,6 +590,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
   // minima in int32 quanta (exact mode), so a cell is p - w + min(aO, aG) in one
   // IADD3 and no conversion; otherwise fp32.
   using CT = std::conditional_t<IW, int, float>;
+
   constexpr int kRectUnroll = IW ? 2 : 1;
   struct Acc { CT b0, b1; int a0, a1; };              // running minima {cost, argj} of t0 / t1
   const int hw = lane >> 4;
@@ -598,7 +610,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
   // the round needs no predicate.
   const int igrp = lane >> 3;
   const uint32_t ibase_s = ring_s + ((igrp & 1) ? 0u : ring_b1<DP, SPARSE>()) + (uint32_t)(((lane & 7) - 4) * 4);
-  const int iwt = (int)a.wt[(lane & 7) + 4];   // cap - Pair at offset (lane & 7) - 3
+  const int iwt = (int)a.wt[(lane & 7) + 4] * kIWS;   // cap - Pair at offset (lane & 7) - 3
   auto rect_run = [&](float (&rr)[4 * NR], int j0, int nsteps, const Tg& tg, Acc& acc) {
     // sparse band round: f = drp - 1 + boff always lands in the buffer or its
     // guards (no range test; zero-weight lanes write back their value)
@@ -616,12 +628,12 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
       return unpack_row(q[0], q[1]);
     };
     auto cell = [&](const RowU& r, int j, int thA, int thB, int f, CT p, CT w, CT& best, int& argj) {
-      if constexpr (IW) {              // records hold int32 quanta (bits in the float fields)
+      if constexpr (IW) {              // records hold scaled int32 quanta (bits in the float fields)
         const int aO = (f > r.ordthr) ? __float_as_int(r.AO1) : __float_as_int(r.AO0);
         const int aG = (f >= thA) ? __float_as_int(r.AGh)
                                   : ((f < thB) ? __float_as_int(r.AGl) : __float_as_int(r.AGm));
-        const int cand = p - w + min(aO, aG);
-        if (cand < best) { best = cand; argj = j; }
+        best = min(best, p - w + min(aO, aG));   // (cost x 32) | bottom offset: run minimum
+        (void)argj; (void)j;
       } else {
         float aO = (f > r.ordthr) ? r.AO1 : r.AO0;
         float aG = (f >= thA) ? r.AGh : ((f < thB) ? r.AGl : r.AGm);
@@ -637,6 +649,8 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
     auto band_i = [&](int drp) {
       atomicAdd(shp<int>(ibase_s + 4u * (uint32_t)drp), -iwt);
     };
+    // IW: the run's packed minima of t0 / t1 (decoded into acc at the end)
+    int m0 = 0x7fffffff, m1 = 0x7fffffff;
     RowU r = rowj(j0 + hw);
     if constexpr (SPARSE && IW) {
       // both buffers := W_{j0-1} (int32); then buffer 1 = W_{j0}, buffer 0 = W_{j0+1}
@@ -687,8 +701,13 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
         const uint32_t wb = SPARSE ? wbuf_s : ring_s + (hw ? ((2 + 2 * half) & 3) : ((1 + 2 * half) & 3)) * DP * 4u;
         const CT p0 = *shp<const CT>(tg.pp0 + 4u * f0), p1 = *shp<const CT>(tg.pp1 + 4u * f1);
         const CT w0 = *shp<const CT>(wb + 4u * f0), w1 = *shp<const CT>(wb + 4u * f1);
-        cell(r, jm, thA, thB, f0, p0, w0, acc.b0, acc.a0);
-        cell(r, jm, thA, thB, f1, p1, w1, acc.b1, acc.a1);
+        if constexpr (IW) {
+          cell(r, jm, thA, thB, f0, p0, w0, m0, acc.a0);
+          cell(r, jm, thA, thB, f1, p1, w1, m1, acc.a1);
+        } else {
+          cell(r, jm, thA, thB, f0, p0, w0, acc.b0, acc.a0);
+          cell(r, jm, thA, thB, f1, p1, w1, acc.b1, acc.a1);
+        }
         if constexpr (SPARSE && IW) {
           __syncwarp();
           band_i(igrp == 1 ? n.drp : r.drp);       // W_jA -> W_{jA+2}, W_{jA+1} -> W_{jA+3}
@@ -707,6 +726,17 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
         __syncwarp();
       }
     }
+    if constexpr (IW) {
+      // a run lies inside one 32-row block: bottom = block base + low bits; runs
+      // come in increasing j per warp, so an equal cost keeps the earlier bottom
+      const int jb = ((j0 - 1) & ~31) + 1;
+      auto fold = [&](int m, CT& best, int& argj) {
+        const int c = m >> 5;            // arithmetic: floor((cost x 32 + off) / 32) = cost
+        if (m != 0x7fffffff && c < best) { best = c; argj = jb + (m & 31); }
+      };
+      fold(m0, acc.b0, acc.a0);
+      fold(m1, acc.b1, acc.a1);
+    }
   };
   // The step's result of target lane (t = lane): the two halves' minima merged,
   // ties to the lower bottom (the first in bottom order, L#17).
@@ -717,7 +747,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
     int ma = hw ? acc.a1 : acc.a0;
     if (sb < mb || (sb == mb && sa < ma)) { mb = sb; ma = sa; }
     float mf;
-    if constexpr (IW) mf = (mb == 0x7fffffff) ? INF : (float)mb;   // exact: |mb| < 2^24
+    if constexpr (IW) mf = (mb >= (1 << 24)) ? INF : (float)mb;   // exact: finite |mb| < 2^24
     else mf = mb;
     return make_float2(mf, __int_as_float(ma));
   };
@@ -892,7 +922,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
         if (idx < ncell && k < h) {
           int f = span_f(rkx - ryx, rky - ryy, smem, Dm1);
           const CT* pv = reinterpret_cast<const CT*>(cs.priv);
-          float data = (float)(pv[kp * (DP + 1) + f] - pv[jp * (DP + 1) + f]) + capQ * (float)(kp - jp);
+          float data = (float)((pv[kp * (DP + 1) + f] - pv[jp * (DP + 1) + f]) / (IW ? kIWS : 1)) + capQ * (float)(kp - jp);
           const int jr = K0b + jp + 1;
           const int2 th = thrS[jr];
           const float pen = (f >= th.x) ? a.kGO_hi : ((f < th.y) ? a.kGO_lo : a.kGO_mid);
@@ -926,7 +956,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
       int rargj = 0x7fffffff;
       if (w == 1) {
         int f = span_f(Tk, N4k, smem, Dm1);
-        rbest = (float)reinterpret_cast<const CT*>(pp)[f] + a.piFirstO;   // shifted by -cap*(k+1)
+        rbest = (float)(reinterpret_cast<const CT*>(pp)[f] / (IW ? kIWS : 1)) + a.piFirstO;   // shifted by -cap*(k+1)
         rargj = 0;
       }
       cs.part[w * 32 + lane] = make_float2(rbest, __int_as_float(rargj));
@@ -1086,7 +1116,11 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
         // shifted by -cap*(k+1)) and the index table
         if (k < h) {
           const float sh = capQ * (float)(k + 1);
-          auto rb = [](float x) { return IW ? (uint32_t)__float2int_rn(x) : __float_as_uint(x); };   // IW: int32 quanta
+          // IW: int32 quanta x 32 with (j - 1) & 31 = k & 31 of row j = k + 1 in the low bits
+          auto rb = [&](float x) {
+            if constexpr (IW) return (uint32_t)((x >= 16777216.f ? kIWBig : __float2int_rn(x) * kIWS) + (k & 31));
+            else return __float_as_uint(x);
+          };
           cs.rec[2 * (k + 1)] = make_uint4(rb((best + a.kOO_lo) - sh), rb((best + a.kOO_hi) - sh),
                                            rb((CGk + a.kGO_mid) - sh), rb((CGk + a.kGO_hi) - sh));
           uint32_t* ry = reinterpret_cast<uint32_t*>(cs.rec + 2 * (k + 1) + 1);
@@ -1122,8 +1156,8 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
                 r0.x, r1.x, r0.y, r1.y};
         if (w == 1 && hw == 0) {       // j = 0: first stixel spans 0..k (Eq. 5)
           const CT pf = IW ? (CT)__float2int_rn(a.piFirstO) : (CT)a.piFirstO;
-          acc.b0 = reinterpret_cast<const CT*>(pp0)[span_f(r0.x, r0.y, smem, Dm1)] + pf;
-          acc.b1 = reinterpret_cast<const CT*>(pp1)[span_f(r1.x, r1.y, smem, Dm1)] + pf;
+          acc.b0 = reinterpret_cast<const CT*>(pp0)[span_f(r0.x, r0.y, smem, Dm1)] / (IW ? kIWS : 1) + pf;
+          acc.b1 = reinterpret_cast<const CT*>(pp1)[span_f(r1.x, r1.y, smem, Dm1)] / (IW ? kIWS : 1) + pf;
           acc.a0 = acc.a1 = 0;
         }
         // full chunks m <= b-1: their records (rows <= 32 b) were final before block b
