@@ -151,6 +151,24 @@ int stixels_create(const stixels_params* params, int width, int height, int max_
 int stixels_query(const stixels_handle* h, int* n_cols, int* cap);
 
 /*
+ * The DP kernel variant stixels_create chose for this model (diagnostics and
+ * tests).  Any pointer may be NULL.
+ *   variant     : STIXELS_DP_DENSE   fp32, dense W-row ring (pair-cost band > 7)
+ *                 STIXELS_DP_SPARSE  fp32, sparse band rounds (band <= 7)
+ *                 STIXELS_DP_PAIR2D  fp32, sigma_O(f) / sigma_G(v) tables (NEXT f2)
+ *                 STIXELS_DP_INT32   int32 quanta, atomic band rounds (band <= 3,
+ *                                    exact mode: cost_frac_bits > 0)
+ *   dp_slots    : object-mean slots per W-row (128 for D <= 128, else 256)
+ *   cols_per_cta: column groups per CTA (one CTA per SM) at a full batch
+ * Errors: ARG (h NULL).
+ */
+#define STIXELS_DP_DENSE 0
+#define STIXELS_DP_SPARSE 1
+#define STIXELS_DP_PAIR2D 2
+#define STIXELS_DP_INT32 3
+int stixels_query_kernel(const stixels_handle* h, int* variant, int* dp_slots, int* cols_per_cta);
+
+/*
  * Run the whole hot path on `batch` frames, asynchronously on the handle's stream.
  *   d_disp    : device, [batch][height][row_pitch_bytes], U8/U16 per params.
  *   d_out     : device, [batch][n_cols][cap] stixel_t; entries >= count are

@@ -511,6 +511,16 @@ int stixels_query(const stixels_handle* h, int* n_cols, int* cap) {
   return STIXELS_OK;
 }
 
+int stixels_query_kernel(const stixels_handle* h, int* variant, int* dp_slots, int* cols_per_cta) {
+  if (!h) return STIXELS_ERR_ARG;
+  if (variant)
+    *variant = h->pair2d ? STIXELS_DP_PAIR2D : h->iw ? STIXELS_DP_INT32 : h->sparse ? STIXELS_DP_SPARSE
+                                                                                  : STIXELS_DP_DENSE;
+  if (dp_slots) *dp_slots = h->dp_slots;
+  if (cols_per_cta) *cols_per_cta = h->cols_per_cta;
+  return STIXELS_OK;
+}
+
 static int launch_reduce(stixels_handle* h, const void* d_disp, int64_t pitch, int batch,
                          uint16_t* d_cols, cudaStream_t s) {
   ReduceArgs r;

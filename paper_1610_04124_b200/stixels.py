@@ -71,6 +71,7 @@ def lib() -> ctypes.CDLL:
         L.stixels_default_params.argtypes = [P(Params)]
         L.stixels_create.argtypes = [P(Params), i32, i32, i32, i32, vp, P(vp)]
         L.stixels_query.argtypes = [vp, P(i32), P(i32)]
+        L.stixels_query_kernel.argtypes = [vp, P(i32), P(i32), P(i32)]
         L.stixels_compute.argtypes = [vp, vp, i64, i32, vp, vp, vp]
         L.stixels_compute_host.argtypes = [vp, vp, i64, i32, vp, vp, vp]
         L.stixels_reduce.argtypes = [vp, vp, i64, i32, vp]
@@ -86,7 +87,11 @@ def lib() -> ctypes.CDLL:
     return _lib
 
 
-EXPORTS = ("stixels_default_params", "stixels_create", "stixels_query", "stixels_compute",
+DP_DENSE, DP_SPARSE, DP_PAIR2D, DP_INT32 = 0, 1, 2, 3   # stixels_query_kernel variants
+
+
+EXPORTS = ("stixels_default_params", "stixels_create", "stixels_query", "stixels_query_kernel",
+           "stixels_compute",
            "stixels_compute_host", "stixels_reduce", "stixels_solve", "stixels_sync",
            "stixels_last_launch_count", "stixels_destroy", "stixels_error_string",
            "stixels_last_error")
@@ -157,6 +162,11 @@ class Handle:
         n, c = ctypes.c_int(), ctypes.c_int()
         _check(lib().stixels_query(h, ctypes.byref(n), ctypes.byref(c)), h)
         self.n_cols, self.cap = n.value, c.value
+        v, ds, cpc = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        _check(lib().stixels_query_kernel(h, ctypes.byref(v), ctypes.byref(ds), ctypes.byref(cpc)), h)
+        # DP kernel variant (DP_DENSE / DP_SPARSE / DP_PAIR2D / DP_INT32), W-row slots,
+        # column groups per CTA
+        self.dp_variant, self.dp_slots, self.cols_per_cta = v.value, ds.value, cpc.value
         self.bpp = 2 if params.disp_format == U16 else 1
 
     # -- allocation helpers (torch device memory) --------------------------

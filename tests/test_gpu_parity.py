@@ -195,6 +195,24 @@ def test_c2_frames_exact():
     assert hd.last_launch_count() == 2
 
 
+def test_dp_variants_exact():
+    """Each DP kernel variant stixels_create picks is exact against
+    the oracle: the int32 atomic-band path (band <= 3, the default model), the
+    fp32 sparse band rounds (band 4..7) and the fp32 dense W-row ring (band > 7),
+    chosen here through sigma_O; continuous mode never takes the int32 path."""
+    from paper_1610_04124_b200 import stixels as S
+    frames = _frames_c2(2, seed0=2600, W=320, H=200)
+    seen = {}
+    for sig_o in (1.0, 1.6, 2.2, 3.0, 4.5, 6.0):
+        p = mp.make(sigma=(2.0, sig_o, 0.5))
+        g, gc, cnt, hd = _assert_exact(p, frames)
+        seen.setdefault(hd.dp_variant, sig_o)
+    assert seen.get(S.DP_INT32) == 1.0
+    assert {S.DP_INT32, S.DP_SPARSE, S.DP_DENSE} <= set(seen), seen
+    _, _, _, hd = run_gpu(mp.make(cost_frac_bits=0), frames[:1])
+    assert hd.dp_variant == S.DP_SPARSE
+
+
 @pytest.mark.parametrize("H,W,D,s", [(1, 40, 16, 5), (31, 64, 16, 3), (32, 50, 64, 5),
                                      (33, 61, 128, 1), (65, 96, 200, 7), (100, 70, 256, 10)])
 def test_shapes_and_disparity_ranges_exact(H, W, D, s):
@@ -290,7 +308,7 @@ def test_capacity_overflow_reported():
 
 
 def test_host_path_matches_device_path():
-    frames = _frames_c2(70, seed0=5000, W=200, H=150)   # > one 64-frame chunk
+    frames = _frames_c2(70, seed0=5000, W=200, H=150)   # several host-path stages
     p = mp.make(ground_slope=0.6)
     a, ac, an, _ = run_gpu(p, frames)
     b, bc, bn, _ = run_gpu(p, frames, host=True)
