@@ -370,6 +370,7 @@ def main():
     del pool_t
     params = S.params_from_dict(p, H_IMG)
     hd = S.Handle(params, W_IMG, H_IMG, B, device=local, stream=stream)
+    dp_variant = hd.dp_variant
     out, cnt, cost = hd.alloc_outputs(B)
     cols = torch.empty((B, hd.n_cols, H_IMG), dtype=torch.int16, device=dev)
     torch.cuda.synchronize()
@@ -520,13 +521,20 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": max_ms / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "i32" if dp_variant == S.DP_INT32 else "f32",
+            "dtype_note": ("exact-mode cost quanta (2^-q nat, L#22): int32 in the rectangle cells, "
+                           "integer-valued fp32 in the serial triangle chain"
+                           if dp_variant == S.DP_INT32 else "exact-mode cost quanta in fp32 (L#22)"),
             "data": "synthetic",
             "config": {"workload": f"C3: batch of {B} frames 1024x440 per GPU, w=5, D=128, "
                                    "u16 disparities (4 frac bits), exact-mode costs q=11",
                        "frames_per_gpu_per_step": B, "distinct_seeded_frames": len(pool),
                        "l2": "inputs 3.7 GB per step >> 126 MB L2 (no flush needed)",
-                       "parallelism": f"frames sharded over {world} GPU(s), no collective"},
+                       "parallelism": f"frames sharded over {world} GPU(s), no collective",
+                       "dp_kernel": {S.DP_DENSE: "fp32 dense W-row ring", S.DP_SPARSE: "fp32 sparse bands",
+                                     S.DP_PAIR2D: "fp32 f2 tables",
+                                     S.DP_INT32: "int32 quanta, atomic band rounds"}[dp_variant]},
             "cells_per_s": cells_per_frame() * frames_total / (max_ms / 1000.0),
             "stage_ms": {"reduce": statistics.mean(red), "dp": dp_ms},
             "stage_share": {"reduce": sum(red) / total_ms, "dp": sum(dp) / total_ms},
