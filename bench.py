@@ -179,7 +179,7 @@ def cpu_baseline(p, pool, frames_req=0):
         run_oracle(p, pool[np.arange(n) % len(pool)], threads=threads)
         dt = time.perf_counter() - t0
     return {"value": n / dt, "unit": "frames/s", "cores": threads, "kind": "oracle",
-            "sample": f"{n} frames of C3 (1024x440, w=5, D=128; the {len(pool)}-frame pool repeated), oracle prefix mode O(h^2), "
+            "sample": f"{n} frames of C3 (1024x440, w=5, D=128{'; the pool of ' + str(len(pool)) + ' repeated' if n > len(pool) else ''}), oracle prefix mode O(h^2), "
                       f"double precision, OpenMP over columns, {threads} threads, {dt:.1f} s"}
 
 
