@@ -16,9 +16,13 @@
  * examples, prefix == direct summation, brute-force enumeration of
  * every labelled segmentation for h <= 8, textbook optimal partitioning for the
  * object-only special case, h = 1 and on-ground-model closed forms, invariants,
- * synthetic-scene recovery.  The numeric values of the prior model are a reading
- * (L#1: the paper defers them to [PfeifferThesis]) and are therefore
- * pinned only by self-consistency and brute force.
+ * synthetic-scene recovery, the prior reading against hand-computed quanta of
+ * every branch (tests/golden/prior_reading.json: BIC, gravity / diving at their
+ * exact boundaries, the ordering direction, forbidden pairs), and the Eq. 6
+ * greedy-predecessor recurrence against an independent plain-Python statement
+ * (tests/eq6_plain.py).  The numeric VALUES of the prior probabilities are a
+ * reading (L#1: the paper defers them to [PfeifferThesis]); their
+ * structure is pinned by the golden file.
  */
 #include <math.h>
 #include <stdint.h>

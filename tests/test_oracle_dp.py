@@ -122,9 +122,14 @@ def test_h1_is_argmin_of_base_costs():
         col = random_col(rng, 1, D, invalid=0.2)
         st, cost = orc.solve_column(m, col, mode=1)
         f = orc.span_mean(m, col, 0, 0)
-        base = [orc.cost_ground(m, col[0], 0) + orc.prior_first(m, G),
-                orc.cost_object(m, col[0], f) + orc.prior_first(m, O),
-                orc.cost_sky(m, col[0]) + orc.prior_first(m, S)]
+        # first-stixel priors from the reading (L#1, golden prior_reading.json),
+        # not from the oracle: -ln p_first[c] - ln p_exist, quantised
+        first = [math.inf if m.p_first[c] <= 0 else
+                 float(round(2048 * (-math.log(m.p_first[c]) - math.log(m.p_exist))))
+                 for c in range(3)]
+        base = [orc.cost_ground(m, col[0], 0) + first[G],
+                orc.cost_object(m, col[0], f) + first[O],
+                orc.cost_sky(m, col[0]) + first[S]]
         assert cost == min(base)
         assert st == [(0, 0, int(np.argmin(base)), st[0][3])]
 
@@ -189,8 +194,10 @@ def test_object_only_reduces_to_optimal_partitioning():
             f = mean(j, k)
             return sum(orc.cost_object(m, int(col[v]), f) for v in range(j, k + 1))
 
-        beta = orc.prior_trans(m, O, 0, O, 1, 0)     # constant when p_ord = 0.5
-        first = orc.prior_first(m, O)
+        # from the reading (L#1), not the oracle: trans O->O + BIC + ordering
+        # (-ln 0.5 on either branch when p_ord = 0.5); first O + BIC
+        beta = round(2048 * (-math.log(m.p_exist))) + round(2048 * -math.log(0.5))
+        first = round(2048 * (-math.log(0.5) - math.log(m.p_exist)))
         want, cuts = _optimal_partitioning(seg, h, beta, first)
         st, cost = orc.solve_column(m, col, mode=1)
         assert cost == want
@@ -278,3 +285,38 @@ def test_noisy_scene_detection_rate():
         d, t = _detection(sc, st, 5)
         det += d; tot += t
     assert tot > 0 and det / tot >= 0.9, (det, tot)
+
+
+def test_dp_equals_plain_python_recurrence_with_ordering():
+    """with the ordering prior active the oracle's DP equals an
+    independent re-implementation of the greedy-predecessor recurrence of Eq. 6
+    (P:129 'the stixel at the end of the segmentation associated with each
+    minimum cost'; tests/eq6_plain.py shares no code with the C
+    oracle), exactly, on random tiny columns with random priors -- including
+    columns where that recurrence is strictly worse than the MAP (L#18)."""
+    from tests import eq6_plain
+    rng = np.random.default_rng(61)
+    cases = []
+    for i in range(240):
+        h = int(rng.integers(1, 11))
+        D = int(rng.integers(4, 24))
+        m = random_model(rng, h, D, ordering=True)
+        m.p_ord = float(rng.choice([0.02, 0.1, 0.3]))
+        cases.append((m, random_col(rng, h, D, invalid=float(rng.choice([0.0, 0.1, 0.4])))))
+    greedy = 0                         # columns where DP > MAP (searched, not assumed)
+    for i in range(1500):
+        h = int(rng.integers(3, 8))
+        D = int(rng.integers(8, 24))
+        m = random_model(rng, h, D, ordering=True)
+        m.p_ord = 0.02
+        col = random_col(rng, h, D, invalid=0.0)
+        if orc.solve_column(m, col)[1] > orc.bruteforce(m, col)[1]:
+            cases.append((m, col))
+            greedy += 1
+    assert greedy >= 3
+    for i, (m, col) in enumerate(cases):
+        st, cost = orc.solve_column(m, col, mode=1)
+        pc, pst = eq6_plain.solve(m, col)
+        assert cost == pc, (i, cost, pc)
+        assert [(a, b, c) for a, b, c, _ in st] == [(a, b, c) for a, b, c, _ in pst], i
+        assert all(d == f for (_, _, c, d), (_, _, _, f) in zip(st, pst) if c == O)

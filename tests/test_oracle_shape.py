@@ -1,0 +1,81 @@
+"""Two more pins of the oracle, CPU only:
+
+* complexity shape: the Eq. 5-6 DP costs O(h^2) per column and is linear in the
+  number of columns (P:157 'O(h^2) ... for each column', P:287 'linear with the
+  image width and quadratic with the height');
+* exact mode (L#22, q = 11) against the paper-literal continuous Eq. 4: on C2
+  frames the column costs agree within north_star's 1e-4 relative, and every
+  column whose list differs is co-optimal under the continuous model (its
+  exact-mode segmentation re-scores within 1e-4 of the continuous minimum).
+"""
+import math
+import time
+
+import numpy as np
+
+from inputs import synth
+from oracle import oracle as orc
+from tests import modelparams as mp
+
+
+def _time_frame(m, cols, reps=5):
+    best = math.inf
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        orc.solve_frame(m, cols, mode=1, threads=1)
+        best = min(best, time.perf_counter() - t0)
+    return best
+
+
+def _slope(xs, ts):
+    return float(np.polyfit(np.log(xs), np.log(ts), 1)[0])
+
+
+def test_complexity_shape():
+    """h-exponent in [1.8, 2.3], column exponent in [0.9, 1.2] (S:583 bounds on
+    P:157 / P:287).  D is small so the O(D h) per-column table build of prefix
+    mode does not mask the O(h^2) DP; one thread, best of 5."""
+    rng = np.random.default_rng(3)
+    D = 8
+
+    def cols_for(n, h):
+        c = rng.integers(0, D * 256, (n, h)).astype(np.int32)
+        c[rng.random((n, h)) < 0.05] = -1
+        return c
+
+    hs = [96, 192, 384]
+    th = [_time_frame(orc.Model(h=h, D=D), cols_for(12, h)) for h in hs]
+    # the same 8 columns tiled, so only the column count changes
+    base = cols_for(8, 192)
+    ns = [8, 24, 64]
+    tn = [_time_frame(orc.Model(h=192, D=D), np.tile(base, (n // 8, 1))) for n in ns]
+    eh, en = _slope(hs, th), _slope(ns, tn)
+    assert 1.8 <= eh <= 2.3, (eh, th)
+    assert 0.9 <= en <= 1.2, (en, tn)
+
+
+def test_exact_mode_within_tolerance_of_continuous():
+    """L#22 stands on this property: the integer-quanta model (q = 11) that the
+    GPU reproduces bit for bit is the paper's continuous Eq. 4 model
+    up to north_star's tolerance, on 4 C2-distribution frames (1024x440, w=5,
+    D=128; 816 columns)."""
+    p = mp.make()
+    H, W, D = 440, 1024, 128
+    frames = synth.frames(2, 4, W, H, D)
+    m_ex = mp.oracle_model(p, H)
+    m_ct = mp.oracle_model(mp.make(cost_frac_bits=0), H)
+    differ = 0
+    for f in frames:
+        cols = orc.reduce(f, 5, 4, 0xFFFF, D)
+        st_e, c_e = orc.solve_frame(m_ex, cols)
+        st_c, c_c = orc.solve_frame(m_ct, cols)
+        for c in range(cols.shape[0]):
+            ce = c_e[c] * 2.0 ** -11
+            assert abs(ce - c_c[c]) <= 1e-4 * c_c[c], (c, ce, c_c[c])
+            if [s[:3] for s in st_e[c]] != [s[:3] for s in st_c[c]] or \
+                    [s[3] for s in st_e[c]] != [s[3] for s in st_c[c]]:
+                differ += 1
+                r = orc.rescore(m_ct, cols[c], st_e[c])
+                assert abs(r - c_c[c]) <= 1e-4 * c_c[c], (c, r, c_c[c])
+    # the property is not vacuous: quantisation does move some decisions
+    assert differ > 0
