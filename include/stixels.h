@@ -112,9 +112,11 @@ typedef struct stixels_params {
          read by stixels_create only; NULL = the per-class constant sigma[]) --- */
   const float* sigma_object_f; /* D entries: sigma_O of the object disparity f;
                                   Pair[f][d] becomes a genuine D x D table.
-                                  Its band (|d - f| with Pair < cap) must be <= 7
-                                  disparities, else UNSUPPORTED                   */
-  const float* sigma_ground_v; /* height entries: sigma_G of model row v           */
+                                  Band (|d - f| with Pair < cap) <= 7: sparse band
+                                  rounds; wider: a dense W-row ring over the table */
+  const float* sigma_ground_v; /* height entries: sigma_G of model row v; either
+                                  table selects the 2-D (PAIR2D) kernels, a missing
+                                  sigma_object_f meaning the constant sigma[1]     */
 } stixels_params;
 
 /* One output stixel (L#19): rows [bottom, top] (bottom <= top, model
@@ -139,7 +141,7 @@ int stixels_default_params(stixels_params* p);
  * |f - d| form, per-row ground model and gravity thresholds, prior constants),
  * upload them to `device`, and allocate the workspace for up to `max_batch`
  * frames of width x height.
- *   width >= s, 1 <= height <= 1024, max_batch >= 1.
+ *   width >= s, 1 <= height <= 1024, 1 <= max_batch <= 65535.
  *   cuda_stream: a cudaStream_t (NULL = the legacy default stream).
  * On success *out owns all tables and workspace.  Errors: ARG, PARAM,
  * UNSUPPORTED (height, D, shared memory, exact-mode range), CUDA.
@@ -155,7 +157,9 @@ int stixels_query(const stixels_handle* h, int* n_cols, int* cap);
  * tests).  Any pointer may be NULL.
  *   variant     : STIXELS_DP_DENSE   fp32, dense W-row ring (pair-cost band > 7)
  *                 STIXELS_DP_SPARSE  fp32, sparse band rounds (band <= 7)
- *                 STIXELS_DP_PAIR2D  fp32, sigma_O(f) / sigma_G(v) tables (NEXT f2)
+ *                 STIXELS_DP_PAIR2D  fp32, sigma_O(f) / sigma_G(v) tables (NEXT f2),
+ *                                    sparse band rounds (band <= 7)
+ *                 STIXELS_DP_PAIR2D_DENSE  the same, dense ring (band > 7)
  *                 STIXELS_DP_INT32   int32 quanta, atomic band rounds (band <= 3,
  *                                    exact mode: cost_frac_bits > 0)
  *   dp_slots    : object-mean slots per W-row (128 for D <= 128, else 256)
@@ -166,6 +170,7 @@ int stixels_query(const stixels_handle* h, int* n_cols, int* cap);
 #define STIXELS_DP_SPARSE 1
 #define STIXELS_DP_PAIR2D 2
 #define STIXELS_DP_INT32 3
+#define STIXELS_DP_PAIR2D_DENSE 4
 int stixels_query_kernel(const stixels_handle* h, int* variant, int* dp_slots, int* cols_per_cta);
 
 /*
@@ -187,8 +192,10 @@ int stixels_compute(stixels_handle* h, const void* d_disp, int64_t row_pitch_byt
 /*
  * End-to-end variant with HOST buffers (pinned memory recommended): copies the
  * inputs host->device and the outputs device->host in chunks of the workspace
- * batch, overlapping copies with compute on two internal streams, and
- * synchronises before returning.  Same layouts as stixels_compute.
+ * batch, overlapping copies with compute on two internal streams (each with its
+ * own DP scratch; both start after work already queued on the handle's stream),
+ * and synchronises before returning.  Same layouts as stixels_compute; the host
+ * row pitch must be a multiple of the pixel size (else ARG).
  */
 int stixels_compute_host(stixels_handle* h, const void* h_disp, int64_t row_pitch_bytes,
                          int batch, stixel_t* h_out, int32_t* h_count, float* h_col_cost);

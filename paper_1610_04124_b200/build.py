@@ -9,6 +9,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libstixels.so")
 SOURCES = [os.path.join(CSRC, f) for f in ("api.cu", "kernels.cuh")]
 HEADER = os.path.join(os.path.dirname(HERE), "include", "stixels.h")
+AB_DIR = os.path.join(os.path.dirname(HERE), "scripts", "ab")   # diagnostic / A/B builds
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -34,14 +35,16 @@ def stale() -> bool:
 def build(force: bool = False, verbose: bool = False, trace: bool = False,
           variant: str | None = None, src: str | None = None) -> str:
     """trace=True builds the diagnostic phase-timeline variant libstixels_trace.so
-    (-DSTX_TRACE; scripts/trace_phases.py); variant=name builds libstixels_<name>.so
-    (from the api.cu at `src` if given) for A/B timing.  Neither is loaded by the
-    product (see stixels.lib)."""
+    (-DSTX_TRACE; scripts/trace_phases.py); variant=name builds
+    scripts/ab/libstixels_<name>.so (from the api.cu at `src` if given) for A/B
+    timing.  Neither is loaded by the product: only an explicit
+    stixels.use_library(path) (bench.py --lib, the scripts) binds them."""
     out = LIB
     if trace:
-        out = os.path.join(HERE, "libstixels_trace.so")
+        out = os.path.join(AB_DIR, "libstixels_trace.so")
     elif variant:
-        out = os.path.join(HERE, f"libstixels_{variant}.so")
+        out = os.path.join(AB_DIR, f"libstixels_{variant}.so")
+    os.makedirs(os.path.dirname(out), exist_ok=True)
     if out == LIB and not force and not stale():
         return LIB
     cmd = [nvcc()] + NVCC_FLAGS + (["-DSTX_TRACE"] if trace else []) + [

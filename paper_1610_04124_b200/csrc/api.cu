@@ -39,10 +39,15 @@ struct stixels_handle {
   int* d_dgR = nullptr;
   uint32_t* d_thr = nullptr;
   int* d_overflow = nullptr;
-  float* d_scratch = nullptr;
+  float* d_scratch = nullptr;   // per-column-slot DP scratch of h->stream (and hs[0])
+  size_t scratch_bytes = 0;
   uint16_t* d_cols = nullptr;
-  // host-buffer path (lazily allocated)
+  // host-buffer path (lazily allocated): two stage streams, each with its own DP
+  // scratch (hs[0] shares d_scratch with h->stream, which it waits for; hs[1] has
+  // hscratch1), so DP launches of consecutive stages may overlap on the SMs
   cudaStream_t hs[2] = {nullptr, nullptr};
+  float* hscratch1 = nullptr;
+  cudaEvent_t ev_entry = nullptr;
   uint8_t* hin[2] = {nullptr, nullptr};
   stixel_t* hout[2] = {nullptr, nullptr};
   int32_t* hcnt[2] = {nullptr, nullptr};
@@ -131,6 +136,8 @@ bool prob_ok(float x) { return std::isfinite(x) && x >= 0.f && x <= 1.f; }
 int validate(const stixels_params* p, int W, int H, int max_batch, std::string& msg) {
   if (!p) { msg = "params is NULL"; return STIXELS_ERR_ARG; }
   if (H < 1 || W < 1 || max_batch < 1) { msg = "width, height and max_batch must be >= 1"; return STIXELS_ERR_ARG; }
+  // the reduction grid carries the frame index in gridDim.z (<= 65535)
+  if (max_batch > 65535) { msg = "max_batch > 65535 not supported"; return STIXELS_ERR_UNSUPPORTED; }
   if (p->stixel_width < 1) { msg = "stixel_width must be >= 1 (S:56)"; return STIXELS_ERR_PARAM; }
   if (W < p->stixel_width) { msg = "width < stixel_width gives no column (S:125)"; return STIXELS_ERR_ARG; }
   if (p->stixel_width > 512) { msg = "stixel_width > 512 not supported"; return STIXELS_ERR_UNSUPPORTED; }
@@ -223,6 +230,8 @@ const char* stixels_last_error(const stixels_handle* h) {
 static void free_all(stixels_handle* h) {
   cudaFree(h->d_E); cudaFree(h->d_E2); cudaFree(h->d_WT); cudaFree(h->d_M2); cudaFree(h->d_gG); cudaFree(h->d_gS);
   cudaFree(h->d_dgR); cudaFree(h->d_thr); cudaFree(h->d_overflow); cudaFree(h->d_cols); cudaFree(h->d_scratch);
+  cudaFree(h->hscratch1);
+  if (h->ev_entry) cudaEventDestroy(h->ev_entry);
   for (int i = 0; i < 2; ++i) {
     cudaFree(h->hin[i]); cudaFree(h->hout[i]); cudaFree(h->hcnt[i]); cudaFree(h->hcost[i]);
     cudaFree(h->hcols[i]);
@@ -336,7 +345,7 @@ int stixels_create(const stixels_params* params, int width, int height, int max_
         E2[(size_t)d * DPv + f] = (float)x;
         if (x != 0.0) band = std::max(band, std::abs(d - f));
       }
-    if (band > 7) return bail(STIXELS_ERR_UNSUPPORTED, "sigma_object_f: the pair-cost band exceeds 7 disparities");
+    // band > 7 (a wide sigma_O(f)): the dense W-row ring reads whole rows of E2
     WT.assign((size_t)(DPv + 17) * 16, 0.f);        // [wt_rows<DP>()][16]
     for (int d = 0; d <= D; ++d)                    // row drp = d + 1, lane offset o = f - d + 7
       for (int o = 0; o < 15; ++o) {
@@ -430,10 +439,10 @@ int stixels_create(const stixels_params* params, int width, int height, int max_
   int optin = (int)prop.sharedMemPerBlockOptin;
   auto kfun = [&]() -> const void* {
     if (DPv == 128)
-      return pair2d ? (const void*)dp_kernel<128, true, true>
+      return pair2d ? (sparse ? (const void*)dp_kernel<128, true, true> : (const void*)dp_kernel<128, false, true>)
              : iw   ? (const void*)dp_kernel<128, true, false, true>
              : sparse ? (const void*)dp_kernel<128, true, false> : (const void*)dp_kernel<128, false, false>;
-    return pair2d ? (const void*)dp_kernel<256, true, true>
+    return pair2d ? (sparse ? (const void*)dp_kernel<256, true, true> : (const void*)dp_kernel<256, false, true>)
            : iw   ? (const void*)dp_kernel<256, true, false, true>
            : sparse ? (const void*)dp_kernel<256, true, false> : (const void*)dp_kernel<256, false, false>;
   };
@@ -441,7 +450,7 @@ int stixels_create(const stixels_params* params, int width, int height, int max_
                       : (sparse ? col_smem_bytes<256, true>(height) : col_smem_bytes<256, false>(height));
   int sb = stx::kM2Pad + al16((height + 1) * 4) + (sparse ? stx::e_copies<true>() : stx::e_copies<false>()) * esz * 4 +
            al16(kTri * 2) +   // pad, M2, E copies, triangle decode
-           (pair2d ? (DPv + 17) * 16 * 4 : 0) +  // NEXT f2 band weights
+           (pair2d && sparse ? (DPv + 17) * 16 * 4 : 0) +  // NEXT f2 band weights
            al16(height * 8);                     // gravity thresholds per row
   int cpc = std::min(4, (optin - sb) / cb);   // columns per CTA (4 warps each)
   if (cpc < 1) return bail(STIXELS_ERR_UNSUPPORTED, "per-column shared memory exceeds the SM");
@@ -475,7 +484,7 @@ int stixels_create(const stixels_params* params, int width, int height, int max_
       (e = alloc((void**)&h->d_dgR, dgR.size() * 4)) != cudaSuccess ||
       (e = alloc((void**)&h->d_thr, thrg.size() * 4)) != cudaSuccess ||
       (e = alloc((void**)&h->d_overflow, 4)) != cudaSuccess ||
-      (e = alloc((void**)&h->d_scratch, (size_t)h->grid * cpc * 4 *
+      (e = alloc((void**)&h->d_scratch, h->scratch_bytes = (size_t)h->grid * cpc * 4 *
                         (DPv == 128 ? col_scratch_floats<128>(height) : col_scratch_floats<256>(height)))) != cudaSuccess ||
       (e = alloc((void**)&h->d_cols, (size_t)max_batch * h->n_cols * height * 2)) != cudaSuccess)
     return bail(STIXELS_ERR_CUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e));
@@ -514,8 +523,8 @@ int stixels_query(const stixels_handle* h, int* n_cols, int* cap) {
 int stixels_query_kernel(const stixels_handle* h, int* variant, int* dp_slots, int* cols_per_cta) {
   if (!h) return STIXELS_ERR_ARG;
   if (variant)
-    *variant = h->pair2d ? STIXELS_DP_PAIR2D : h->iw ? STIXELS_DP_INT32 : h->sparse ? STIXELS_DP_SPARSE
-                                                                                  : STIXELS_DP_DENSE;
+    *variant = h->pair2d ? (h->sparse ? STIXELS_DP_PAIR2D : STIXELS_DP_PAIR2D_DENSE)
+               : h->iw ? STIXELS_DP_INT32 : h->sparse ? STIXELS_DP_SPARSE : STIXELS_DP_DENSE;
   if (dp_slots) *dp_slots = h->dp_slots;
   if (cols_per_cta) *cols_per_cta = h->cols_per_cta;
   return STIXELS_OK;
@@ -550,8 +559,9 @@ static int launch_reduce(stixels_handle* h, const void* d_disp, int64_t pitch, i
 }
 
 static int launch_dp(stixels_handle* h, const uint16_t* d_cols, int batch, stixel_t* d_out,
-                     int32_t* d_count, float* d_cost, cudaStream_t s) {
+                     int32_t* d_count, float* d_cost, cudaStream_t s, float* scratch) {
   DPArgs A = h->args;
+  A.scratch = scratch;
   A.cols = d_cols; A.out = d_out; A.count = d_count; A.col_cost = d_cost;
   A.items = batch * h->n_cols;
   // Column groups per CTA: the full count when the batch fills the GPU; fewer when
@@ -563,12 +573,14 @@ static int launch_dp(stixels_handle* h, const uint16_t* d_cols, int batch, stixe
   int grid = std::min(h->grid, (A.items + C - 1) / C);
   const int threads = C * kCW * 32;
   if (h->dp_slots == 128) {
-    if (h->pair2d) dp_kernel<128, true, true><<<grid, threads, smem, s>>>(A);
+    if (h->pair2d && h->sparse) dp_kernel<128, true, true><<<grid, threads, smem, s>>>(A);
+    else if (h->pair2d) dp_kernel<128, false, true><<<grid, threads, smem, s>>>(A);
     else if (h->iw) dp_kernel<128, true, false, true><<<grid, threads, smem, s>>>(A);
     else if (h->sparse) dp_kernel<128, true, false><<<grid, threads, smem, s>>>(A);
     else dp_kernel<128, false, false><<<grid, threads, smem, s>>>(A);
   } else {
-    if (h->pair2d) dp_kernel<256, true, true><<<grid, threads, smem, s>>>(A);
+    if (h->pair2d && h->sparse) dp_kernel<256, true, true><<<grid, threads, smem, s>>>(A);
+    else if (h->pair2d) dp_kernel<256, false, true><<<grid, threads, smem, s>>>(A);
     else if (h->iw) dp_kernel<256, true, false, true><<<grid, threads, smem, s>>>(A);
     else if (h->sparse) dp_kernel<256, true, false><<<grid, threads, smem, s>>>(A);
     else dp_kernel<256, false, false><<<grid, threads, smem, s>>>(A);
@@ -604,7 +616,7 @@ int stixels_solve(stixels_handle* h, const uint16_t* d_cols, int batch, stixel_t
     return fail(h, STIXELS_ERR_ARG, "bad pointer or batch");
   cudaSetDevice(h->device);
   h->launches = 1;
-  return launch_dp(h, d_cols, batch, d_out, d_count, d_cost, h->stream);
+  return launch_dp(h, d_cols, batch, d_out, d_count, d_cost, h->stream, h->d_scratch);
 }
 
 int stixels_compute(stixels_handle* h, const void* d_disp, int64_t pitch, int batch,
@@ -616,7 +628,7 @@ int stixels_compute(stixels_handle* h, const void* d_disp, int64_t pitch, int ba
   h->launches = 2;
   st = launch_reduce(h, d_disp, pitch, batch, h->d_cols, h->stream);
   if (st) return st;
-  return launch_dp(h, h->d_cols, batch, d_out, d_count, d_cost, h->stream);
+  return launch_dp(h, h->d_cols, batch, d_out, d_count, d_cost, h->stream, h->d_scratch);
 }
 
 int stixels_compute_host(stixels_handle* h, const void* h_disp, int64_t pitch, int batch,
@@ -624,9 +636,11 @@ int stixels_compute_host(stixels_handle* h, const void* h_disp, int64_t pitch, i
   if (!h) return STIXELS_ERR_ARG;
   if (h->sticky) return h->sticky;
   int bpp = bytes_per_px(h->p.disp_format);
-  if (!h_disp || !h_out || !h_count || batch < 1 || pitch < (int64_t)h->W * bpp)
+  if (!h_disp || !h_out || !h_count || batch < 1 || pitch < (int64_t)h->W * bpp || (pitch % bpp))
     return fail(h, STIXELS_ERR_ARG, "bad host pointer, batch or pitch");
   cudaSetDevice(h->device);
+  if (!h->hscratch1) CU(cudaMalloc(&h->hscratch1, h->scratch_bytes), h);
+  if (!h->ev_entry) CU(cudaEventCreateWithFlags(&h->ev_entry, cudaEventDisableTiming), h);
   // frames per H2D / compute / D2H stage: about 32, chosen so that the stage's
   // columns fill the column slots evenly (1024x440: 29 frames = 5916 columns =
   // 10 per slot on 588 of 592 slots; 32 frames would leave 16 slots a 12th column)
@@ -657,6 +671,11 @@ int stixels_compute_host(stixels_handle* h, const void* h_disp, int64_t pitch, i
     h->h_chunk = chunk;
     h->h_pitch = pitch;
   }
+  // work already queued on the handle's stream (stixels_compute) uses d_scratch:
+  // both stage streams start after it
+  CU(cudaEventRecord(h->ev_entry, h->stream), h);
+  CU(cudaStreamWaitEvent(h->hs[0], h->ev_entry, 0), h);
+  CU(cudaStreamWaitEvent(h->hs[1], h->ev_entry, 0), h);
   int launches = 0;
   for (int b0 = 0, it = 0; b0 < batch; b0 += chunk, ++it) {
     const int nb = std::min(chunk, batch - b0);
@@ -667,7 +686,8 @@ int stixels_compute_host(stixels_handle* h, const void* h_disp, int64_t pitch, i
                        cudaMemcpyHostToDevice, s), h);
     int st = launch_reduce(h, h->hin[i], pitch, nb, h->hcols[i], s);
     if (st) return st;
-    st = launch_dp(h, h->hcols[i], nb, h->hout[i], h->hcnt[i], h->hcost[i], s);
+    st = launch_dp(h, h->hcols[i], nb, h->hout[i], h->hcnt[i], h->hcost[i], s,
+                   i ? h->hscratch1 : h->d_scratch);
     if (st) return st;
     launches += 2;
     CU(cudaMemcpyAsync(h_out + (size_t)b0 * h->n_cols * h->cap, h->hout[i],

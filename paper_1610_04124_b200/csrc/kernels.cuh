@@ -521,10 +521,10 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
     else E[i] = a.E[i];
   }
   float* WT = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(tri_jk) + al16(kTri * 2));
-  if constexpr (PAIR2D)
+  if constexpr (PAIR2D && SPARSE)
     for (int i = threadIdx.x; i < wt_rows<DP>() * 16; i += blockDim.x) WT[i] = a.WTg[i];
   // gravity thresholds {thrA1[j], thrB[j]} per row (one LDS.64 per row in the rectangle)
-  int2* thrS = reinterpret_cast<int2*>(reinterpret_cast<uint8_t*>(WT) + (PAIR2D ? wt_rows<DP>() * 16 * 4 : 0));
+  int2* thrS = reinterpret_cast<int2*>(reinterpret_cast<uint8_t*>(WT) + (PAIR2D && SPARSE ? wt_rows<DP>() * 16 * 4 : 0));
   for (int i = threadIdx.x; i < h; i += blockDim.x) thrS[i] = make_int2(a.thrA1[i], a.thrB[i]);
   const uint32_t thr_s = (uint32_t)__cvta_generic_to_shared(thrS);
   for (int jp = 0; jp < 31; ++jp)                 // triangle cell index -> (j', k')
@@ -556,11 +556,13 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
   // dead lanes (lane 15/31, zero weight) get an offset that puts every f out of range
   // ---- helpers --------------------------------------------------------------
   // dense W-row step: rr += E'[.][d_src] for f = 4*lane.. (+128 r); store to slot
+  // (PAIR2D: the row E'[d_src][.] of the 2-D table, from global memory / L2)
   auto ring_step = [&](float (&rr)[4 * NR], int row_src, int slot) {
-    uint32_t e = cs.eo[row_src] & 0xffffu;
+    uint32_t e = PAIR2D ? cs.eo[row_src] >> 16 : cs.eo[row_src] & 0xffffu;
 #pragma unroll
     for (int r = 0; r < NR; ++r) {
-      float4 x = *reinterpret_cast<const float4*>(Eb + e + 16 * lane + 512 * r);
+      float4 x = PAIR2D ? __ldg(reinterpret_cast<const float4*>(a.E2g + e * DP) + lane + 32 * r)
+                        : *reinterpret_cast<const float4*>(Eb + e + 16 * lane + 512 * r);
       fadd2_inplace(rr[4 * r + 0], rr[4 * r + 1], x.x, x.y);
       fadd2_inplace(rr[4 * r + 2], rr[4 * r + 3], x.z, x.w);
       *reinterpret_cast<float4*>(ringw + slot * DP + 4 * lane + 128 * r) =

@@ -54,14 +54,24 @@ assert STIXEL_DTYPE.itemsize == 12
 _lib = None
 
 
+_lib_path = LIB
+
+
+def use_library(path: str) -> None:
+    """Explicitly bind another build of the same ABI (A/B timing: bench.py --lib,
+    scripts/ab_variant.py).  Must precede the first call into the library; the
+    product path never calls it."""
+    global _lib_path
+    if _lib is not None and os.path.abspath(path) != os.path.abspath(_lib_path):
+        raise RuntimeError("library already loaded from " + _lib_path)
+    _lib_path = path
+
+
 def lib() -> ctypes.CDLL:
     """Load libstixels.so (built in-tree by paper_1610_04124_b200.build).  Raises if absent."""
     global _lib
     if _lib is None:
-        # STIXELS_LIB_VARIANT=name loads the A/B build libstixels_<name>.so (same
-        # directory; scripts only) instead of the product library
-        var = os.environ.get("STIXELS_LIB_VARIANT")
-        path = LIB if not var else os.path.join(os.path.dirname(LIB), f"libstixels_{var}.so")
+        path = _lib_path
         if not os.path.exists(path):
             raise RuntimeError(f"{path} not built; run paper_1610_04124_b200.build.build() "
                                "(there is no CPU fallback)")
@@ -87,7 +97,8 @@ def lib() -> ctypes.CDLL:
     return _lib
 
 
-DP_DENSE, DP_SPARSE, DP_PAIR2D, DP_INT32 = 0, 1, 2, 3   # stixels_query_kernel variants
+# stixels_query_kernel variants
+DP_DENSE, DP_SPARSE, DP_PAIR2D, DP_INT32, DP_PAIR2D_DENSE = 0, 1, 2, 3, 4
 
 
 EXPORTS = ("stixels_default_params", "stixels_create", "stixels_query", "stixels_query_kernel",
@@ -167,7 +178,7 @@ class Handle:
         # DP kernel variant (DP_DENSE / DP_SPARSE / DP_PAIR2D / DP_INT32), W-row slots,
         # column groups per CTA
         self.dp_variant, self.dp_slots, self.cols_per_cta = v.value, ds.value, cpc.value
-        self.bpp = 2 if params.disp_format == U16 else 1
+        self.bpp = {U8: 1, U16: 2, F32: 4}[params.disp_format]
 
     # -- allocation helpers (torch device memory) --------------------------
     def alloc_outputs(self, batch: int):

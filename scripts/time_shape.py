@@ -1,6 +1,6 @@
 #!/usr/bin/env python3
-"""Frames/s of the whole path at one shape (A/B helper; honours STIXELS_LIB_VARIANT).
-usage: time_shape.py W H [s] [D] [batch]"""
+"""Frames/s of the whole path at one shape (A/B helper).
+usage: time_shape.py W H [s] [D] [batch] [lib.so]"""
 import os
 import sys
 
@@ -17,6 +17,8 @@ W, H = int(sys.argv[1]), int(sys.argv[2])
 s = int(sys.argv[3]) if len(sys.argv) > 3 else 5
 D = int(sys.argv[4]) if len(sys.argv) > 4 else 128
 B = int(sys.argv[5]) if len(sys.argv) > 5 else 1024
+if len(sys.argv) > 6:
+    S.use_library(sys.argv[6])
 p = mp.make(max_disparity=D, stixel_width=s)
 pool = np.stack([synth.frame(4, i, W, H, D) for i in range(8)])
 disp = torch.from_numpy(pool.view(np.int16)).cuda()[torch.arange(B) % 8]

@@ -276,26 +276,29 @@ def test_random_priors_exact():
 
 
 def test_continuous_mode_tolerance():
-    """cost_frac_bits = 0: fp32 Eq. 4 vs double.  Column cost within 1e-4
-    relative; lists identical except where the GPU's segmentation is co-optimal
-    (re-scored within 1e-4 of the oracle minimum), BASELINE north_star."""
+    """cost_frac_bits = 0 (the paper-literal fp32 Eq. 4) vs double on
+    3 C2 frames: column cost within 1e-4 relative; full stixel tuples (bounds,
+    class, disparity) identical except where the GPU's segmentation is
+    co-optimal (re-scored within 1e-4 of the oracle minimum), BASELINE
+    north_star."""
     from oracle import oracle as orc
-    frames = _frames_c2(1)
+    frames = _frames_c2(3, seed0=2100)
     p = mp.make(cost_frac_bits=0)
     g, gc, cnt, hd = run_gpu(p, frames)
     o, oc = run_oracle(p, frames)
     m = mp.oracle_model(p, 440)
-    cols = orc.reduce(frames[0], 5, 4, 0xFFFF, 128)
-    ties = 0
-    for c in range(len(o[0])):
-        assert abs(gc[0][c] - oc[0][c]) <= 1e-4 * abs(oc[0][c])
-        og = [(a, b, k) for a, b, k, _ in o[0][c]]
-        gg = [(a, b, k) for a, b, k, _ in g[0][c]]
-        if og != gg:
-            ties += 1
-            rs = orc.rescore(m, cols[c], [(a, b, k, 0.0) for a, b, k in gg])
-            assert abs(rs - oc[0][c]) <= 1e-4 * abs(oc[0][c])
-    assert ties <= len(o[0]) // 10
+    ties = total = 0
+    for b in range(3):
+        cols = orc.reduce(frames[b], 5, 4, 0xFFFF, 128)
+        for c in range(len(o[b])):
+            total += 1
+            assert abs(gc[b][c] - oc[b][c]) <= 1e-4 * abs(oc[b][c])
+            og = [(a, z, k, float(np.float32(d))) for a, z, k, d in o[b][c]]
+            if og != g[b][c]:
+                ties += 1
+                rs = orc.rescore(m, cols[c], g[b][c])
+                assert abs(rs - oc[b][c]) <= 1e-4 * abs(oc[b][c]), (b, c)
+    assert ties <= total // 10
 
 
 def test_capacity_overflow_reported():
@@ -313,6 +316,79 @@ def test_host_path_matches_device_path():
     a, ac, an, _ = run_gpu(p, frames)
     b, bc, bn, _ = run_gpu(p, frames, host=True)
     assert a == b and (ac == bc).all() and (an == bn).all()
+
+
+def test_host_path_pinned_overlapping_stages():
+    """stixels_compute_host with PINNED buffers (asynchronous copies, so
+    consecutive stages overlap on the GPU) at the GPU-filling C2 shape, 4 stages
+    of 29 frames, right after a device-path call still queued on the handle's
+    stream: byte-identical to the device path, sampled columns exact against
+    the oracle (per-stage DP scratch, entry wait on the stream)."""
+    import torch
+    from oracle import oracle as orc
+    from paper_1610_04124_b200 import stixels as S
+    from tests.gpuharness import compare_exact
+    n = 116
+    pool = _frames_c2(8, seed0=5100)
+    frames = pool[np.arange(n) % 8]
+    p = mp.make()
+    hd = S.Handle(S.params_from_dict(p, 440), 1024, 440, n)
+    dev = torch.from_numpy(frames.view(np.int16)).cuda()
+    o1, c1, k1 = hd.alloc_outputs(n)
+    hin = torch.from_numpy(frames.view(np.int16)).pin_memory()
+    hout = torch.zeros((n, hd.n_cols, hd.cap, 12), dtype=torch.uint8).pin_memory()
+    hcnt = torch.zeros((n, hd.n_cols), dtype=torch.int32).pin_memory()
+    hcost = torch.zeros((n, hd.n_cols), dtype=torch.float32).pin_memory()
+    for rep in range(2):
+        hd.compute(dev, o1, c1, k1)            # queued, not synchronised
+        hd.compute_host_ptr(hin.data_ptr(), 1024 * 2, n, hout.data_ptr(), hcnt.data_ptr(),
+                            hcost.data_ptr())
+        hd.sync()
+        cnt = c1.cpu()
+        assert torch.equal(hcnt, cnt) and torch.equal(hcost, k1.cpu())
+        for f in range(n):                     # entries past count are undefined
+            for c in range(0, hd.n_cols, 7):
+                m = int(cnt[f, c])
+                assert torch.equal(hout[f, c, :m], o1[f, c, :m].cpu())
+    got = S.decode(hout.numpy(), hcnt.numpy())
+    m = mp.oracle_model(p, 440)
+    rng = np.random.default_rng(3)
+    for f in (0, 57, 115):
+        ci = rng.choice(hd.n_cols, 10, replace=False)
+        st, oc = orc.solve_frame(m, orc.reduce(frames[f], 5, 4, 0xFFFF, 128)[ci])
+        assert not compare_exact([[got[f][c] for c in ci]], [hcost.numpy()[f][ci]], [st], [oc], 11)
+
+
+def test_noise_model_wide_band_dense_exact():
+    """NEXT f2 with a wide sigma_O(f) sigmoid (reaching ~5 px, pair-cost band
+    > 7): the dense ring over the 2-D table runs and is exact; a
+    per-row ground table alone with a wide scalar sigma_O also runs (formerly
+    UNSUPPORTED)."""
+    from paper_1610_04124_b200 import stixels as S
+    frames = _frames_c2(2, seed0=2750, W=400, H=220)
+    f = np.arange(128)
+    so = (1.0 + 4.0 / (1.0 + np.exp(-(f - 64) / 12.0))).astype(np.float32)
+    _, sg = _sigma_tables(7, 128, 220)
+    p = mp.make(sigma_object_f=so, sigma_ground_v=sg)
+    _, _, _, hd = _assert_exact(p, frames)
+    assert hd.dp_variant == S.DP_PAIR2D_DENSE
+    p = mp.make(sigma=(2.0, 4.0, 0.5), sigma_ground_v=sg)
+    _, _, _, hd = _assert_exact(p, frames)
+    assert hd.dp_variant == S.DP_PAIR2D_DENSE
+
+
+def test_camera_derived_ground_slope_exact():
+    """ground_slope <= 0: alpha = B cos(theta) / H_cam, theta = atan((c_y -
+    v_hor) / f) (P:63, L#21), computed on both sides independently."""
+    H, W, D = 440, 1024, 128
+    p = mp.make(ground_slope=0.0, focal_px=1200.0, baseline_m=0.5, camera_height_m=1.5,
+                principal_row=250.0)
+    hz = p["horizon_frac"] * H
+    th = np.arctan((p["principal_row"] - hz) / p["focal_px"])
+    alpha = float(p["baseline_m"] * np.cos(th) / p["camera_height_m"])
+    frames = np.stack([synth.render(synth.random_scene(2950 + i, W, H, D, alpha=alpha), 2950 + i)
+                       for i in range(2)])
+    _assert_exact(p, frames)
 
 
 def test_deterministic_bytes():

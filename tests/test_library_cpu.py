@@ -95,18 +95,25 @@ def test_median_width_limit():
 
 
 def test_sigma_tables_validated():
-    """NEXT f2 tables: entries must be finite and > 0; an object band wider than
-    7 disparities is unsupported (checked before any device work)."""
+    """NEXT f2 tables: entries must be finite and > 0 (checked before any device
+    work); a wide object band is accepted (dense ring), so with no device the
+    create gets as far as the CUDA error."""
     from tests import modelparams as mp
     D, H = 64, 120
     bad = np.full(D, 1.0, np.float32)
     bad[5] = 0.0
     assert _create(S.params_from_dict(mp.make(max_disparity=D, sigma_object_f=bad), H), H=H) == S.ERR_PARAM
     wide = np.full(D, 4.0, np.float32)
-    assert _create(S.params_from_dict(mp.make(max_disparity=D, sigma_object_f=wide), H), H=H) == S.ERR_UNSUPPORTED
+    assert _create(S.params_from_dict(mp.make(max_disparity=D, sigma_object_f=wide), H), H=H) == S.ERR_CUDA
     g = np.full(H, 1.0, np.float32)
     g[-1] = np.nan
     assert _create(S.params_from_dict(mp.make(max_disparity=D, sigma_ground_v=g), H), H=H) == S.ERR_PARAM
+
+
+def test_max_batch_limit():
+    """The reduction grid carries frames in gridDim.z: max_batch <= 65535."""
+    p = S.default_params()
+    assert _create(p, B_=65536) == S.ERR_UNSUPPORTED
 
 
 def test_exact_mode_range_guard():
