@@ -4,15 +4,18 @@
 
 One step = one pass of the whole hot path (reduction + DP + backtracking,
 SURVEY 8(a) a1-a7) over one batch of synthetic frames resident in HBM:
-config C3, 4096 frames of 1024x440, w=5, D=128 per rank.  Frames are
-independent, so N ranks each process their own batch (weak scaling, no
-collective on the data path; NCCL only carries the barrier and the max-over-
-ranks timing).
+config C3 (BASELINE configs[2]), 4096 frames of 1024x440, w=5, D=128, split
+into contiguous 4096/N shards over N GPUs (strong scaling; `--weak` gives every
+rank its own 4096).  Frames are independent, so there is no collective
+on the data path; the process group carries only barriers, the max-over-ranks
+timing and, after the timed region, a gather of per-frame output digests (the
+cross-rank identity check of SURVEY 8(e)).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
 Rank 0 prints ONE JSON line.  `--impl reference` times the CPU oracle (the
-reference arm for this paper-only tier) on the host cores.
+reference arm for this paper-only tier) on the host cores; `--cpu-full` runs
+BASELINE.md's oracle plan (C1-C5 samples) and prints its own line.
 """
 from __future__ import annotations
 
@@ -41,13 +44,23 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--batch", type=int, default=4096, help="frames per rank per step")
+    ap.add_argument("--batch", type=int, default=4096,
+                    help="frames per step for the whole job (BASELINE configs[2]: 4096, split "
+                         "4096/N over N GPUs); with --weak: frames per rank")
+    ap.add_argument("--weak", action="store_true",
+                    help="weak scaling: every rank runs its own --batch frames")
     ap.add_argument("--distinct", type=int, default=128, help="distinct seeded frames in the pool")
-    ap.add_argument("--e2e-batch", type=int, default=1024)
+    ap.add_argument("--e2e-batch", type=int, default=1024, help="frames per e2e call (whole job)")
+    ap.add_argument("--e2e-seconds", type=float, default=1.0, help="minimum e2e timed span")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-cont", action="store_true", help="skip the continuous-mode (q=0) leg")
     ap.add_argument("--no-single", action="store_true", help="skip the one-frame latency run")
     ap.add_argument("--cpu-frames", type=int, default=0, help="oracle sample size (0 = auto)")
+    ap.add_argument("--cpu-full", action="store_true",
+                    help="only the oracle baseline plan of BASELINE.md (C1-C5 samples, 1 thread "
+                         "and all cores; one JSON line, no GPU)")
+    ap.add_argument("--lib", default="", help="time another build of the same C ABI (A/B)")
     ap.add_argument("--sweep", action="store_true",
                     help="NEXT f1: resolution / stixel-width sweep with fps/W (one JSON line "
                          "per config; not the driver's bench line)")
@@ -70,15 +83,20 @@ def params_dict():
     return mp.make()
 
 
-def frame_indices(rank, n):
-    """Seeded frame indices of a rank's pool (config 3 = C3): disjoint per rank,
-    since frames are sharded (weak scaling, each rank owns its own batch)."""
-    return [rank * 100000 + i for i in range(n)]
-
-
-def frame_pool(n, rank):
+def frame_pool(n):
+    """The pool of distinct seeded C3 frames (config 3, seeds 3000 + i); global
+    frame g of a step is pool frame g mod n."""
     from inputs import synth
-    return np.stack([synth.frame(3, i, W_IMG, H_IMG, D_MAX) for i in frame_indices(rank, n)])
+    return np.stack([synth.frame(3, i, W_IMG, H_IMG, D_MAX) for i in range(n)])
+
+
+def frame_shard(total, rank, world, weak):
+    """Global frame indices [g0, g1) of this rank: a contiguous 1/N shard of the
+    job's batch (strong scaling, configs[2]), or a whole batch per rank (weak)."""
+    from paper_1610_04124_b200.shard import shard_range
+    if weak:
+        return rank * total, (rank + 1) * total
+    return shard_range(total, rank, world)
 
 
 def max_over_ranks(value, world, device=None):
@@ -162,9 +180,32 @@ def ncu_profile():
         return {}
 
 
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def _oracle_fps(p, frames, threads, W=W_IMG, H=H_IMG):
+    """Frames/s of the oracle (prefix mode, reduction included) on `frames`, and
+    the per-frame seconds."""
+    from tests.gpuharness import run_oracle
+    per = []
+    for f in frames:
+        t0 = time.perf_counter()
+        run_oracle(p, f[None], threads=threads)
+        per.append(time.perf_counter() - t0)
+    return len(per) / sum(per), per
+
+
 def cpu_baseline(p, pool, frames_req=0):
     """The oracle (prefix mode, OpenMP over columns, all host cores) on a bounded
-    sample of the same workload."""
+    sample of the same workload; plus BASELINE.md's C2 figures: the median of 3
+    frames on all cores and on ONE thread (SPEC S:583 bound: < 1 s per frame)."""
     from tests.gpuharness import run_oracle
     from oracle import oracle as orc
     threads = orc.max_threads()
@@ -178,9 +219,56 @@ def cpu_baseline(p, pool, frames_req=0):
         t0 = time.perf_counter()
         run_oracle(p, pool[np.arange(n) % len(pool)], threads=threads)
         dt = time.perf_counter() - t0
+    _, all3 = _oracle_fps(p, pool[:3], threads)
+    _, one3 = _oracle_fps(p, pool[:3], 1)
     return {"value": n / dt, "unit": "frames/s", "cores": threads, "kind": "oracle",
+            "cpu_model": cpu_model(), "os_cpu_count": os.cpu_count(),
             "sample": f"{n} frames of C3 (1024x440, w=5, D=128{'; the pool of ' + str(len(pool)) + ' repeated' if n > len(pool) else ''}), oracle prefix mode O(h^2), "
-                      f"double precision, OpenMP over columns, {threads} threads, {dt:.1f} s"}
+                      f"double precision, OpenMP over columns, {threads} threads, {dt:.1f} s",
+            "c2_median_of_3": {"all_cores_s_per_frame": statistics.median(all3),
+                               "all_cores_fps": 1.0 / statistics.median(all3),
+                               "one_thread_s_per_frame": statistics.median(one3),
+                               "one_thread_fps": 1.0 / statistics.median(one3),
+                               "spec_bound_one_thread_lt_1s": statistics.median(one3) < 1.0},
+            "paper_context": "13.3 fps on a 6-core i7-980X (P:287), other hardware"}
+
+
+def run_cpu_full():
+    """BASELINE.md's oracle plan: C1, C2 (median of 3), C3 (64 frames,
+    extrapolated), C4 (w = 3/5/7/10, 3 frames each), C5 (2 frames), on all host
+    cores, C2 also on one thread.  One JSON line (kept under profiles/)."""
+    from inputs import synth
+    from oracle import oracle as orc
+    from tests import modelparams as mp
+    threads = orc.max_threads()
+    res = {"cpu_baseline_plan": "BASELINE.md", "cpu_model": cpu_model(), "threads": threads,
+           "os_cpu_count": os.cpu_count(), "mode": "oracle prefix O(h^2), double, OpenMP over columns"}
+    sc = synth.c1_scene()
+    c1 = np.stack([synth.render(sc, 1, noise=False)] * 3)
+    fps, per = _oracle_fps(mp.make(max_disparity=32, ground_slope=sc.alpha), c1, threads)
+    res["C1"] = {"fps": fps, "s_per_frame_median": statistics.median(per)}
+    p = mp.make()
+    pool = frame_pool(8)
+    for th, key in ((threads, "C2_all_cores"), (1, "C2_one_thread")):
+        fps, per = _oracle_fps(p, pool[:3], th)
+        res[key] = {"s_per_frame_median": statistics.median(per), "fps_median": 1 / statistics.median(per),
+                    "frames": 3, "threads": th}
+    from tests.gpuharness import run_oracle
+    t0 = time.perf_counter()
+    run_oracle(p, pool[np.arange(64) % 8], threads=threads)
+    dt = time.perf_counter() - t0
+    res["C3"] = {"fps": 64 / dt, "frames_timed": 64,
+                 "batch_4096_s_extrapolated": 4096 * dt / 64, "note": "extrapolated from 64 frames"}
+    for s in (3, 5, 7, 10):
+        pc = mp.make(stixel_width=s)
+        fps, per = _oracle_fps(pc, pool[:3], threads)
+        res[f"C4_w{s}"] = {"fps": fps, "s_per_frame_median": statistics.median(per), "frames": 3}
+    p5 = mp.make(max_disparity=256, ground_slope=0.35, cost_frac_bits=10)
+    c5 = np.stack([synth.frame(5, i, 2048, 1024, 256, alpha=0.35) for i in range(2)])
+    fps, per = _oracle_fps(p5, c5, threads)
+    res["C5"] = {"fps": fps, "s_per_frame_median": statistics.median(per), "frames": 2,
+                 "W": 2048, "H": 1024, "D": 256}
+    print(json.dumps(res), flush=True)
 
 
 def run_reference(args, rank, world):
@@ -189,7 +277,7 @@ def run_reference(args, rank, world):
     if rank != 0:
         return
     p = params_dict()
-    pool = frame_pool(4, 0)
+    pool = frame_pool(4)
     from tests.gpuharness import run_oracle
     from oracle import oracle as orc
     threads = orc.max_threads()
@@ -206,11 +294,13 @@ def run_reference(args, rank, world):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "frames/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1000 * tot / args.steps, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": 1000 * tot / args.steps, "higher_is_better": True,
+        "scaling": "weak" if args.weak else "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": "C3: batch of 1024x440 frames, w=5, D=128 (bounded sample: "
                                f"{per_step} frames per step)", "frames_per_step": per_step},
         "cpu_baseline": {"value": value, "unit": "frames/s", "cores": threads, "kind": "oracle",
+                         "cpu_model": cpu_model(),
                          "sample": f"{per_step} frames per step, oracle prefix mode, "
                                    f"{threads} threads"},
         "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0,
@@ -331,24 +421,79 @@ def run_quality(n, local):
     print(json.dumps(line), flush=True)
 
 
+def sampled_parity(p, S, hd, pool, pool_idx, out, cnt, cost, frames, ncols=8, seed=1):
+    """Sampled columns of the given output frames against the oracle: exact mode
+    -> identical lists and costs; continuous mode (q = 0) -> north_star
+    tolerance (cost within 1e-4 relative, lists identical or co-optimal by
+    re-score).  Returns (checked, bad)."""
+    from oracle import oracle as orc
+    from tests import modelparams as mp
+    from tests.gpuharness import compare_exact
+    rng = np.random.default_rng(seed)
+    m = mp.oracle_model(p, H_IMG)
+    fr = list(frames)
+    out_h, cnt_h, cost_h = out[fr].cpu().numpy(), cnt[fr].cpu().numpy(), cost[fr].cpu().numpy()
+    got = S.decode(out_h, cnt_h)
+    bad = checked = 0
+    for i, f in enumerate(fr):
+        cidx = rng.choice(hd.n_cols, ncols, replace=False)
+        rcols = orc.reduce(pool[pool_idx[f]], S_W, 4, 0xFFFF, D_MAX)[cidx]
+        st, oc = orc.solve_frame(m, rcols)
+        checked += len(cidx)
+        if p["cost_frac_bits"]:
+            bad += len(compare_exact([[got[i][c] for c in cidx]], [cost_h[i][cidx]], [st], [oc],
+                                     p["cost_frac_bits"]))
+            continue
+        for j, c in enumerate(cidx):
+            if abs(cost_h[i][c] - oc[j]) > 1e-4 * abs(oc[j]):
+                bad += 1
+            elif [(a, b, k, float(np.float32(d))) for a, b, k, d in st[j]] != got[i][c] and \
+                    abs(orc.rescore(m, rcols[j], got[i][c]) - oc[j]) > 1e-4 * abs(oc[j]):
+                bad += 1
+    return checked, bad
+
+
 def main():
     args = parse()
     rank, world, local = dist_env()
+    if args.cpu_full:
+        if rank == 0:
+            run_cpu_full()
+        return
     import torch
     import torch.distributed as dist
-    if world > 1 and not dist.is_initialized():
-        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
     if args.impl == "reference":
+        if world > 1 and not dist.is_initialized():
+            dist.init_process_group("gloo")
         run_reference(args, rank, world)
         if dist.is_initialized():
             dist.destroy_process_group()
         return
 
     assert torch.cuda.is_available(), "bench.py (ours) needs a GPU"
+    # one process per GPU over NCCL.  (Only when there are fewer GPUs than ranks --
+    # a multi-rank smoke run on a 1-GPU box -- do ranks share devices; NCCL cannot
+    # put two ranks on one GPU, so the host bookkeeping then goes over gloo.)
+    shared = torch.cuda.device_count() < world
+    local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1 and not dist.is_initialized():
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+    cdev = torch.device("cpu") if shared else dev      # device of collective tensors
+    # build once: rank 0 rebuilds a stale library while the other ranks wait
     from paper_1610_04124_b200 import build as b
-    b.build()
+    if rank == 0:
+        b.build()
+    if world > 1:
+        dist.barrier()
     from paper_1610_04124_b200 import stixels as S
+    from paper_1610_04124_b200.shard import gather_shards
+    if args.lib:
+        S.use_library(args.lib)
     if args.sweep:
         if rank == 0:
             run_sweep(args, local)
@@ -359,10 +504,11 @@ def main():
         return
 
     p = params_dict()
-    B = args.batch
-    pool = frame_pool(min(args.distinct, B), rank)
-    idx = np.arange(B) % len(pool)
-    dev = torch.device("cuda", local)
+    g0, g1 = frame_shard(args.batch, rank, world, args.weak)
+    B = g1 - g0                                   # this rank's frames per step
+    job_frames = args.batch * (world if args.weak else 1)
+    pool = frame_pool(min(args.distinct, job_frames))
+    idx = np.arange(g0, g1) % len(pool)           # pool frame of each local frame
     stream = torch.cuda.Stream(dev)
     disp = torch.empty((B, H_IMG, W_IMG), dtype=torch.int16, device=dev)
     pool_t = torch.from_numpy(pool.view(np.int16)).to(dev)
@@ -375,61 +521,80 @@ def main():
     cols = torch.empty((B, hd.n_cols, H_IMG), dtype=torch.int16, device=dev)
     torch.cuda.synchronize()
 
-    def step(evs=None):
+    def step(h, evs=None):
         with torch.cuda.stream(stream):
             if evs:
                 evs[0].record(stream)
-            hd.reduce(disp, cols)
+            h.reduce(disp, cols)
             if evs:
                 evs[1].record(stream)
-            hd.solve(cols, out, cnt, cost)
+            h.solve(cols, out, cnt, cost)
             if evs:
                 evs[2].record(stream)
 
+    def timed(h, steps, sample_clocks):
+        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(steps)]
+        sampler = ClockSampler(local)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        if sample_clocks:
+            sampler.start()
+            time.sleep(0.3)
+        for k in range(steps):
+            step(h, evs[k])
+        torch.cuda.synchronize()
+        clocks = sampler.stop() if sample_clocks else None
+        if world > 1:
+            dist.barrier()
+        red = [e[0].elapsed_time(e[1]) for e in evs]
+        dp = [e[1].elapsed_time(e[2]) for e in evs]
+        return red, dp, clocks
+
     for _ in range(args.warmup):
-        step()
+        step(hd)
     torch.cuda.synchronize()
 
     # sampled parity against the oracle at full size, same launch configuration
     parity = "skipped"
     if rank == 0:
-        from tests.gpuharness import compare_exact
-        from oracle import oracle as orc
-        from tests import modelparams as mp
         rng = np.random.default_rng(1)
-        fr = rng.choice(B, 4, replace=False)
-        m = mp.oracle_model(p, H_IMG)
-        out_h, cnt_h, cost_h = out[fr].cpu().numpy(), cnt[fr].cpu().numpy(), cost[fr].cpu().numpy()
-        got = S.decode(out_h, cnt_h)
-        bad = 0
-        for i, f in enumerate(fr):
-            cidx = rng.choice(hd.n_cols, 8, replace=False)
-            rcols = orc.reduce(pool[idx[f]], S_W, 4, 0xFFFF, D_MAX)[cidx]
-            st, oc = orc.solve_frame(m, rcols)
-            bad += len(compare_exact([[got[i][c] for c in cidx]], [cost_h[i][cidx]], [st], [oc],
-                                     p["cost_frac_bits"]))
-        parity = "exact (32 sampled columns)" if bad == 0 else f"MISMATCH on {bad}/32 columns"
+        n_chk, bad = sampled_parity(p, S, hd, pool, idx, out, cnt, cost,
+                                    rng.choice(B, min(4, B), replace=False))
+        parity = f"exact ({n_chk} sampled columns)" if bad == 0 else f"MISMATCH on {bad}/{n_chk} columns"
 
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
-    sampler = ClockSampler(local)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    sampler.start()
-    time.sleep(0.3)
-    for k in range(args.steps):
-        step(evs[k])
-    torch.cuda.synchronize()
-    clocks = sampler.stop()
-    if world > 1:
-        dist.barrier()
-    red = [e[0].elapsed_time(e[1]) for e in evs]
-    dp = [e[1].elapsed_time(e[2]) for e in evs]
+    red, dp, clocks = timed(hd, args.steps, True)
     step_ms = [r + d for r, d in zip(red, dp)]
     total_ms = sum(step_ms)
-    max_ms = max_over_ranks(total_ms, world, dev)
-    frames_total = B * world * args.steps
-    value = aggregate_value(B, args.steps, world, max_ms)
+    max_ms = max_over_ranks(total_ms, world, cdev)
+    steps_max = [max_over_ranks(x, world, cdev) for x in step_ms]
+    value = aggregate_value(job_frames, args.steps, 1, max_ms)
+
+    # cross-rank identity (8(e)): frames that are the same pool frame give the same
+    # bytes on every rank; per-frame digests gathered over the process group
+    # (NCCL at N > 1) after the timed region
+    ident = None
+    with torch.no_grad():
+        dig = torch.empty((B, 3), dtype=torch.int64, device=dev)
+        wts = torch.randint(1, 1 << 20, (hd.cap, 3), generator=torch.Generator().manual_seed(7),
+                            dtype=torch.int64).to(dev)
+        ar = torch.arange(hd.cap, device=dev)
+        for a0 in range(0, B, 128):
+            a1 = min(B, a0 + 128)
+            o = out[a0:a1].view(torch.int32).view(a1 - a0, hd.n_cols, hd.cap, 3).to(torch.int64)
+            mask = (ar[None, None, :] < cnt[a0:a1, :, None]).to(torch.int64)
+            dig[a0:a1, 0] = (o * wts * mask[..., None]).sum((1, 2, 3))
+            dig[a0:a1, 1] = cnt[a0:a1].to(torch.int64).sum(1)
+            dig[a0:a1, 2] = cost[a0:a1].double().sum(1).mul(2048.0).round().to(torch.int64)
+        if not args.weak:
+            full = gather_shards(dig.to(cdev), args.batch, rank, world)
+            if rank == 0:
+                pidx = np.arange(args.batch) % len(pool)
+                fd = full.cpu().numpy()
+                ok = all((fd[pidx == q] == fd[q]).all() for q in range(len(pool)))
+                ident = {"check": "frames equal to the same pool frame have identical output "
+                                  "digests across the whole job (all ranks gathered)",
+                         "frames": args.batch, "ranks": world, "ok": bool(ok)}
 
     # roofline of the dominant kernel (the DP): algorithmic ALU ops / duration
     peaks = measured_peaks()
@@ -458,36 +623,84 @@ def main():
                    "frac": red_bytes / (red_ms / 1000.0) / 1e9 / hbm_peak,
                    "bytes_per_launch": red_bytes}
 
-    # end-to-end through the C ABI with host buffers (pinned), copies included
+    # the paper-literal continuous Eq. 4 (cost_frac_bits = 0, fp32 sparse bands) on
+    # the same batch: its own timing, roofline and tolerance parity
+    cont = None
+    if not args.no_cont:
+        pc = dict(p, cost_frac_bits=0)
+        hdc = S.Handle(S.params_from_dict(pc, H_IMG), W_IMG, H_IMG, B, device=local, stream=stream)
+        for _ in range(args.warmup):
+            step(hdc)
+        torch.cuda.synchronize()
+        cpar = "skipped"
+        if rank == 0:
+            rng = np.random.default_rng(2)
+            n_chk, bad = sampled_parity(pc, S, hdc, pool, idx, out, cnt, cost,
+                                        rng.choice(B, min(4, B), replace=False), seed=2)
+            cpar = (f"north_star tolerance ({n_chk} sampled columns)" if bad == 0
+                    else f"MISMATCH on {bad}/{n_chk} columns")
+        cred, cdp, _ = timed(hdc, max(2, min(args.steps, 3)), False)
+        cmax = max_over_ranks(sum(cred) + sum(cdp), world, cdev)
+        cdp_ms = statistics.mean(cdp)
+        cach = cells * ALG_OPS_PER_CELL / (cdp_ms / 1000.0) / 1e12
+        cont = {"value": aggregate_value(job_frames, len(cdp), 1, cmax), "unit": "frames/s",
+                "dtype": "f32", "cost_frac_bits": 0,
+                "dp_kernel": {S.DP_SPARSE: "fp32 sparse bands", S.DP_DENSE: "fp32 dense W-row ring"}
+                .get(hdc.dp_variant, str(hdc.dp_variant)),
+                "ms_per_step": cmax / len(cdp),
+                "roofline": {"bound": "alu", "achieved": cach, "peak": peak_tops, "unit": "Tops/s",
+                             "frac": cach / peak_tops, "kernel": "dp_kernel (fp32)"},
+                "parity": cpar}
+        hdc.destroy()
+
+    # end-to-end through the C ABI with host buffers (pinned), copies included,
+    # timed over >= --e2e-seconds; sampled parity on its outputs
     e2e = None
     if not args.no_e2e:
-        eb = min(args.e2e_batch, B)
+        e0_, e1_ = frame_shard(args.e2e_batch, rank, world, args.weak)
+        eb = e1_ - e0_
+        eidx = np.arange(e0_, e1_) % len(pool)
         p2 = dict(p, max_stixels=128)
         hd2 = S.Handle(S.params_from_dict(p2, H_IMG), W_IMG, H_IMG, min(eb, 32), device=local,
                        stream=stream)
         hin = torch.empty((eb, H_IMG, W_IMG), dtype=torch.int16).pin_memory()
-        hin.copy_(torch.from_numpy(pool[idx[:eb]].view(np.int16)))
+        hin.copy_(torch.from_numpy(pool[eidx].view(np.int16)))
         hout = torch.empty((eb, hd2.n_cols, hd2.cap, 12), dtype=torch.uint8).pin_memory()
         hcnt = torch.empty((eb, hd2.n_cols), dtype=torch.int32).pin_memory()
         hcost = torch.empty((eb, hd2.n_cols), dtype=torch.float32).pin_memory()
         pitch = W_IMG * 2
-        hd2.compute_host_ptr(hin.data_ptr(), pitch, eb, hout.data_ptr(), hcnt.data_ptr(),
-                             hcost.data_ptr())
-        e_steps = max(1, min(args.steps, 3))
+
+        def call():
+            hd2.compute_host_ptr(hin.data_ptr(), pitch, eb, hout.data_ptr(), hcnt.data_ptr(),
+                                 hcost.data_ptr())
+        call()
+        t0 = time.perf_counter()
+        call()
+        call()
+        one = (time.perf_counter() - t0) / 2
+        e_steps = int(max_over_ranks(max(3, int(np.ceil(1.2 * args.e2e_seconds / max(one, 1e-6)))),
+                                     world, cdev))
+        epar = "skipped"
+        if rank == 0:
+            rng = np.random.default_rng(3)
+            n_chk, bad = sampled_parity(p2, S, hd2, pool, eidx, hout, hcnt, hcost,
+                                        rng.choice(eb, min(3, eb), replace=False), seed=3)
+            epar = f"exact ({n_chk} sampled columns)" if bad == 0 else f"MISMATCH on {bad}/{n_chk} columns"
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(e_steps):
-            hd2.compute_host_ptr(hin.data_ptr(), pitch, eb, hout.data_ptr(), hcnt.data_ptr(),
-                                 hcost.data_ptr())
-        dt = max_over_ranks(time.perf_counter() - t0, world, dev)
-        e2e = {"value": world * eb * e_steps / dt, "unit": "frames/s",
+            call()
+        dt = max_over_ranks(time.perf_counter() - t0, world, cdev)
+        e2e = {"value": args.e2e_batch * (world if args.weak else 1) * e_steps / dt,
+               "unit": "frames/s",
                "h2d_bytes_per_step": eb * H_IMG * pitch,
                "d2h_bytes_per_step": eb * hd2.n_cols * (hd2.cap * 12 + 8),
-               "frames_per_step": eb, "max_stixels": 128,
+               "frames_per_step": eb, "steps": e_steps, "seconds": dt, "max_stixels": 128,
+               "parity": epar,
                "note": "stixels_compute_host: pinned host buffers, ~32-frame stages (29 at 1024x440) on 2 "
-                       "streams, synchronous call; wall clock max over ranks"}
+                       "streams (own DP scratch each), synchronous call; wall clock max over ranks"}
         hd2.destroy()
 
     # BASELINE configs[1]: ONE frame per call (latency; the GPU is mostly idle: 204
@@ -505,7 +718,7 @@ def main():
         with torch.cuda.stream(stream):
             s0.record(stream)
             for i in range(n1):
-                hd1.compute(disp[i:i + 1], o1, c1, k1)
+                hd1.compute(disp[i % B:i % B + 1], o1, c1, k1)
             s1.record(stream)
         torch.cuda.synchronize()
         lat_ms = s0.elapsed_time(s1) / n1
@@ -521,25 +734,35 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": max_ms / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step_median": statistics.median(steps_max), "ms_per_step_min": min(steps_max),
+            "ms_per_step_max": max(steps_max),
+            "higher_is_better": True, "scaling": "weak" if args.weak else "strong",
+            "vs_baseline": None,
             "dtype": "i32" if dp_variant == S.DP_INT32 else "f32",
             "dtype_note": ("exact-mode cost quanta (2^-q nat, L#22): int32 in the rectangle cells, "
                            "integer-valued fp32 in the serial triangle chain"
                            if dp_variant == S.DP_INT32 else "exact-mode cost quanta in fp32 (L#22)"),
             "data": "synthetic",
-            "config": {"workload": f"C3: batch of {B} frames 1024x440 per GPU, w=5, D=128, "
-                                   "u16 disparities (4 frac bits), exact-mode costs q=11",
-                       "frames_per_gpu_per_step": B, "distinct_seeded_frames": len(pool),
-                       "l2": "inputs 3.7 GB per step >> 126 MB L2 (no flush needed)",
-                       "parallelism": f"frames sharded over {world} GPU(s), no collective",
+            "config": {"workload": f"C3: batch of {job_frames} frames 1024x440 per step "
+                                   f"({'per GPU, weak' if args.weak else f'{args.batch}/{world} per GPU'}), "
+                                   "w=5, D=128, u16 disparities (4 frac bits), exact-mode costs q=11",
+                       "frames_per_step": job_frames, "frames_per_gpu_per_step": B,
+                       "distinct_seeded_frames": len(pool),
+                       "l2": f"inputs {B * H_IMG * W_IMG * 2 / 1e9:.2f} GB per GPU per step >> 126 MB L2 "
+                             "(no flush needed)",
+                       "parallelism": f"contiguous frame shards over {world} GPU(s), no collective "
+                                      "on the data path",
                        "dp_kernel": {S.DP_DENSE: "fp32 dense W-row ring", S.DP_SPARSE: "fp32 sparse bands",
-                                     S.DP_PAIR2D: "fp32 f2 tables",
-                                     S.DP_INT32: "int32 quanta, atomic band rounds"}[dp_variant]},
-            "cells_per_s": cells_per_frame() * frames_total / (max_ms / 1000.0),
+                                     S.DP_PAIR2D: "fp32 f2 tables", S.DP_PAIR2D_DENSE: "fp32 f2 dense",
+                                     S.DP_INT32: "int32 quanta, atomic band rounds"}[dp_variant],
+                       "lib": args.lib or "libstixels.so",
+                       "ranks_share_gpus": shared},
+            "cells_per_s": cells_per_frame() * job_frames * args.steps / (max_ms / 1000.0),
             "stage_ms": {"reduce": statistics.mean(red), "dp": dp_ms},
             "stage_share": {"reduce": sum(red) / total_ms, "dp": sum(dp) / total_ms},
-            "roofline": roofline, "k1_roofline": k1_roofline, "cpu_baseline": cpu, "e2e": e2e,
-            "single_frame": single,
+            "roofline": roofline, "k1_roofline": k1_roofline, "continuous": cont,
+            "cpu_baseline": cpu, "e2e": e2e,
+            "single_frame": single, "cross_rank_identity": ident,
             "gpu_launches": 2 * args.steps, "clocks": clocks, "parity": parity,
             "fps_per_watt": (value / world / clocks["power_w"]) if clocks.get("power_w") else None,
         }
