@@ -225,6 +225,9 @@ constexpr int kIWS = 32;
 // is stored as 2^30: p - w <= 0 keeps every candidate built on it below 2^30 (no
 // overflow) and above any finite cost; unscaled costs >= 2^24 read back as INF.
 constexpr int kIWBig = 1 << 30;
+// The serial chain's INF: finite costs are below 2^24 quanta (host check), so
+// x 32 below 2^29; sums of three terms each <= 2^29 cannot overflow.
+constexpr int kChainBig = 1 << 29;
 
 // Diagnostic phase timeline (build with -DSTX_TRACE; scripts/trace_phases.py):
 // CTA 0's column groups record %globaltimer stamps (ns; one clock for all SM
@@ -318,6 +321,10 @@ template <int DP, bool SPARSE>
 __host__ __device__ constexpr uint32_t ring_b1() { return (DP + 48) * 4u; }   // from buffer 0
 template <int DP>
 __host__ __device__ constexpr int no_band() { return DP + 16; }   // drp code: invalid pixel
+// priv row stride (floats): == 3 mod 32, so the two half-warps' gathers of adjacent
+// targets whose means differ by one land in different banks
+template <int DP>
+__host__ __device__ constexpr int priv_stride() { return DP + 3; }
 // E' copies in shared memory: the dense ring reads 4 shifted copies, the sparse
 // path (build only) one.
 template <bool SPARSE>
@@ -326,7 +333,7 @@ __host__ __device__ constexpr int e_copies() { return SPARSE ? 1 : 4; }
 template <int DP, bool SPARSE>
 __host__ __device__ inline int col_smem_bytes(int h) {
   int b = 0;
-  b += al16(32 * (DP + 1) * 4);
+  b += al16(32 * priv_stride<DP>() * 4);
   b += al16(2 * DP * 4);
   b += al16(kCW * ring_stride<DP, SPARSE>() * 4);
   b += kTri * 16;
@@ -348,7 +355,7 @@ __host__ __device__ inline int64_t col_scratch_floats(int h) {
 template <int DP, bool SPARSE>
 __device__ inline ColSmem carve(uint8_t* p, int h) {
   ColSmem w;
-  w.priv = reinterpret_cast<float*>(p); p += al16(32 * (DP + 1) * 4);
+  w.priv = reinterpret_cast<float*>(p); p += al16(32 * priv_stride<DP>() * 4);
   w.seed = reinterpret_cast<float*>(p); p += al16(2 * DP * 4);
   w.ring = reinterpret_cast<float*>(p); p += al16(kCW * ring_stride<DP, SPARSE>() * 4);
   w.cell = reinterpret_cast<float4*>(p); p += kTri * 16;
@@ -502,6 +509,11 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
   const int Dm1 = a.D - 1;
   const int nb = (h + 31) >> 5;
   const float capQ = a.capQ;
+  // IW serial chain: exact-mode costs as int32 quanta x 32 (below kChainBig = 2^29,
+  // L#22's 2^24 bound), INF (a forbidden transition) saturated to kChainBig
+  auto toI = [](float x) { return x >= 16777216.f ? kChainBig : __float2int_rn(x) * kIWS; };
+  const int capI = IW ? __float2int_rn(capQ) * kIWS : 0;
+  const int goHiI = toI(a.kGO_hi), goLoI = toI(a.kGO_lo), goMidI = toI(a.kGO_mid);
   const int bar_col = 1 + cslot;       // 128 threads: whole column group
   const int bar_rect = 1 + C + cslot;  // 96 threads: rectangle warps
   const int bar_x = 1 + 2 * C + cslot; // 96 arrive + 32 sync: next block's priv rows ready
@@ -894,8 +906,8 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
                 } else {
                   fadd2_inplace(fr[c], fr[c + 1], x[r][c], x[r][c + 1]);
                 }
-                *shp<CT>(dst_s + ((i0 + r) * (DP + 1) + 32 * (c0 + c)) * 4u) = fr[c];
-                *shp<CT>(dst_s + ((i0 + r) * (DP + 1) + 32 * (c0 + c) + 32) * 4u) = fr[c + 1];
+                *shp<CT>(dst_s + ((i0 + r) * priv_stride<DP>() + 32 * (c0 + c)) * 4u) = fr[c];
+                *shp<CT>(dst_s + ((i0 + r) * priv_stride<DP>() + 32 * (c0 + c) + 32) * 4u) = fr[c + 1];
               }
             }
           }
@@ -915,6 +927,31 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
       // {T, N4} of the block's rows K0b+1+l in lane l: the cells' row reads become
       // shuffles (the records' 32-byte stride would make them 8-way bank conflicts)
       const uint2 tnl = tn_at(min(K0b + lane + 1, h));
+      if constexpr (IW) {
+        // IW: int32 cells for the packed serial chain.  Warp iteration `it` takes
+        // bottom rows j' = it (targets k' = it+1+l, lanes l < 31-it) and j' = 30-it
+        // (targets k' = l, the other it+1 lanes): 32 cells, two distinct rows.
+        // Cell = {data x 32 | code, min(data + gravity prior, BIG) x 32 | code, f,
+        // f - ord_margin}, code = j' + 1 (the bottom's place in the block, L#17).
+        const int* pv = reinterpret_cast<const int*>(cs.priv);
+        int4* cl = reinterpret_cast<int4*>(cs.cell);
+        const int wq = t0 >> 5, nq = nthr >> 5;       // this warp's index among nq warps
+        for (int it = wq; it < 16; it += nq) {
+          const bool lo = lane < 31 - it;
+          const int jr = lo ? it : 30 - it;
+          const int kp = lo ? it + 1 + lane : lane;
+          const uint32_t ryx = __shfl_sync(0xffffffffu, tnl.x, jr), ryy = __shfl_sync(0xffffffffu, tnl.y, jr);
+          const uint32_t rkx = __shfl_sync(0xffffffffu, tnl.x, kp), rky = __shfl_sync(0xffffffffu, tnl.y, kp);
+          if (kp <= jn) {
+            const int f = span_f(rkx - ryx, rky - ryy, smem, Dm1);
+            const int d = pv[kp * priv_stride<DP>() + f] - pv[jr * priv_stride<DP>() + f] + capI * (kp - jr);
+            const int2 th = thrS[K0b + jr + 1];
+            const int pen = (f >= th.x) ? goHiI : ((f < th.y) ? goLoI : goMidI);
+            const int code = jr + 1;
+            cl[tri_off(jr) + kp - jr - 1] = make_int4(d + code, min(d + pen, kChainBig) + code, f, f - a.ord_margin);
+          }
+        }
+      } else {
       for (int base = t0 - lane; base < ncell; base += nthr) {   // warp-uniform trip count
         const int idx = base + lane;
         const uint32_t jk = tri_jk[min(idx, kTri - 1)];
@@ -925,19 +962,20 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
         if (idx < ncell && k < h) {
           int f = span_f(rkx - ryx, rky - ryy, smem, Dm1);
           const CT* pv = reinterpret_cast<const CT*>(cs.priv);
-          float data = (float)((pv[kp * (DP + 1) + f] - pv[jp * (DP + 1) + f]) / (IW ? kIWS : 1)) + capQ * (float)(kp - jp);
+          float data = (float)((pv[kp * priv_stride<DP>() + f] - pv[jp * priv_stride<DP>() + f]) / (IW ? kIWS : 1)) + capQ * (float)(kp - jp);
           const int jr = K0b + jp + 1;
           const int2 th = thrS[jr];
           const float pen = (f >= th.x) ? a.kGO_hi : ((f < th.y) ? a.kGO_lo : a.kGO_mid);
           cs.cell[idx] = make_float4(data, data + pen, __int_as_float(f), 0.f);
         }
       }
+      }
     };
     // seed of the second half of block bt's newest chunk: W-row K0 + 16 (priv row 15)
     auto copy_seed = [&](int bt) {
       if ((bt << 5) + 32 < h) {          // only needed if a next block exists
         float* sd = cs.seed + (bt & 1) * DP;
-        const float* row = cs.priv + 15 * (DP + 1);
+        const float* row = cs.priv + 15 * priv_stride<DP>();
         for (int f = lane; f < DP; f += 32) sd[f] = row[f];
       }
     };
@@ -954,7 +992,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
       const int kk = lane < h ? lane : h - 1;
       const uint2 rky = tn_at(kk + 1);
       const uint32_t Tk = rky.x, N4k = rky.y;
-      const float* pp = cs.priv + kk * (DP + 1);   // lanes past h: the last row's copy
+      const float* pp = cs.priv + kk * priv_stride<DP>();   // lanes past h: the last row's copy
       float rbest = INF;
       int rargj = 0x7fffffff;
       if (w == 1) {
@@ -1013,20 +1051,66 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
           else argc = (aG <= aO) ? 0 : 1;
         }
         const float kOG = a.kOG;
-        // per row j = K0 + lane: {kOG - PG[j], PG[j+1]} for the in-loop ground chain
-        cs.pgps[lane] = make_float4(kOG - pg0, pg1, 0.f, 0.f);
-        __syncwarp();
-        const float oh = opaque(a.kOO_hi), ol = opaque(a.kOO_lo);
         const int om = a.ord_margin;
-
+        const int jn = min(K0 + 31, h - 1) - K0;
         // Chain state: C_O, C_G and the object mean of the last finalised target.
         // Target K0: all its bottoms were in the rectangle.
         float mg = (K0 == 0) ? a.piFirstG : fminf(MG, cCO + (kOG - pg0));   // lane 0's value
         mg = __shfl_sync(0xffffffffu, mg, 0);
+        int tri_c = 0;                   // IW: the winner's code (0: a bottom before the block)
+        if constexpr (IW) {
+          // Packed int32 chain (exact mode): costs x 32 with the bottom's code j' + 1
+          // in the low 5 bits (0 for the rectangle's winner, whose bottom is lower),
+          // so the first-minimum rule of L#17 is one integer min; argc is
+          // recovered after the scans.
+          int2* pq = reinterpret_cast<int2*>(cs.pgps);
+          pq[lane] = make_int2(toI(kOG - pg0), toI(pg1));
+          __syncwarp();
+          const int oh = toI(a.kOO_hi), ol = toI(a.kOO_lo);
+          const int4* cl = reinterpret_cast<const int4*>(cs.cell);
+          int mgI = toI(mg);
+          int prevCG = toI(__shfl_sync(0xffffffffu, pg1, 0) + mg);
+          int bI = toI(best);
+          int afI = argf;
+          int prevCO = __shfl_sync(0xffffffffu, bI, 0);
+          int prevF = __shfl_sync(0xffffffffu, argf, 0);
+          int rB = __shfl_sync(0xffffffffu, bI, 1);
+          int rF = __shfl_sync(0xffffffffu, argf, 1);
+          int off = 0;                                  // tri_off(jp)
+          STX_STAMP(b, 13);
+          for (int jp = 0; jp < jn; ++jp) {
+            const int2 q = pq[jp + 1];
+            const int4 dcell = cl[off];                 // diagonal cell (bottom j, target j)
+            const int dc = min(dcell.x + prevCO + ((dcell.w > prevF) ? oh : ol), dcell.y + prevCG);
+            const bool take = dc < rB;
+            const int COj = take ? dc : rB;
+            const int Fj = take ? dcell.z : rF;
+            {
+              const int4 lc = cl[off + lane - jp - 1];  // (lanes <= jp read a dead slot)
+              const int cand = min(lc.x + prevCO + ((lc.w > prevF) ? oh : ol), lc.y + prevCG);
+              const bool upd = (lane > jp) && (cand < bI);
+              bI = upd ? cand : bI;
+              afI = upd ? lc.z : afI;
+            }
+            rB = __shfl_sync(0xffffffffu, bI, (jp + 2) & 31);
+            rF = __shfl_sync(0xffffffffu, afI, (jp + 2) & 31);
+            mgI = min(mgI, prevCO + q.x);               // ground chain (value only)
+            prevCG = q.y + mgI;
+            prevCO = min(COj & ~31, kChainBig);
+            prevF = Fj;
+            off += 31 - jp;
+          }
+          best = (bI >= kChainBig) ? INF : (float)(bI >> 5);
+          tri_c = bI & 31;
+          if (tri_c) { argj = K0 + tri_c; argf = afI; }
+        } else {
+        // per row j = K0 + lane: {kOG - PG[j], PG[j+1]} for the in-loop ground chain
+        cs.pgps[lane] = make_float4(kOG - pg0, pg1, 0.f, 0.f);
+        __syncwarp();
+        const float oh = opaque(a.kOO_hi), ol = opaque(a.kOO_lo);
         float prevCG = __shfl_sync(0xffffffffu, pg1, 0) + mg;
         float prevCO = __shfl_sync(0xffffffffu, best, 0);
         int prevF = __shfl_sync(0xffffffffu, argf, 0);
-        const int jn = min(K0 + 31, h - 1) - K0;
         // running minimum (over bottoms < j) of the next target to finalise
         float rB = __shfl_sync(0xffffffffu, best, 1);
         int rF = __shfl_sync(0xffffffffu, argf, 1);
@@ -1073,6 +1157,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
           prevF = Fj;
           off += 31 - jp;
         }
+        }
         STX_STAMP(b, 14);                 // serial: triangle chain done
         // ---- ground / sky argmins and values of the block's rows, as warp scans ----
         // lane l = row j = K0 + l = target k: candidates at bottom j use C[j-1]
@@ -1104,6 +1189,21 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
         }
         if (K0 > 0 && !(vS < MS)) { vS = MS; aS = sj; }
         const float CSk = ps1 + vS;
+        if constexpr (IW) {
+          // predecessor class of a triangle winner (bottom j = K0 + tri_c): G iff
+          // its G candidate is <= its O candidate (L#17), re-evaluated from the
+          // final C_O, C_G and f of row j - 1 (lane tri_c - 1)
+          const int src = max(tri_c - 1, 0);
+          const float pO = __shfl_sync(0xffffffffu, best, src);
+          const float pG = __shfl_sync(0xffffffffu, CGk, src);
+          const int pF = __shfl_sync(0xffffffffu, argf, src);
+          if (tri_c) {
+            const int4 lc = reinterpret_cast<const int4*>(cs.cell)[tri_off(src) + lane - src - 1];
+            const int tO = lc.x + min(toI(pO), kChainBig) + ((lc.w > pF) ? toI(a.kOO_hi) : toI(a.kOO_lo));
+            const int tG = lc.y + toI(pG);
+            argc = (tG <= tO) ? 0 : 1;
+          }
+        }
         // carry to the next block: last row of this block (lane 31, or h-1)
         const int L = min(31, h - 1 - K0);
         MG = __shfl_sync(0xffffffffu, vG, L); gj = __shfl_sync(0xffffffffu, aG, L);
@@ -1153,8 +1253,8 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
         // (targets past h duplicate the last row: only built priv rows are read)
         const int k0 = min(Kn + t0, h - 1), k1 = min(Kn + t1, h - 1);
         const uint2 r0 = tn_at(k0 + 1), r1 = tn_at(k1 + 1);
-        const float* pp0 = cs.priv + (k0 - Kn) * (DP + 1);
-        const float* pp1 = cs.priv + (k1 - Kn) * (DP + 1);
+        const float* pp0 = cs.priv + (k0 - Kn) * priv_stride<DP>();
+        const float* pp1 = cs.priv + (k1 - Kn) * priv_stride<DP>();
         tg = Tg{(uint32_t)__cvta_generic_to_shared(pp0), (uint32_t)__cvta_generic_to_shared(pp1),
                 r0.x, r1.x, r0.y, r1.y};
         if (w == 1 && hw == 0) {       // j = 0: first stixel spans 0..k (Eq. 5)
