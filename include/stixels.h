@@ -220,6 +220,25 @@ int stixels_sync(stixels_handle* h);
 /* Number of kernel launches the last compute/solve/reduce call enqueued. */
 int stixels_last_launch_count(const stixels_handle* h);
 
+/* Shape of the last DP launch (stixels_compute / stixels_solve /
+ * stixels_compute_host), for tests and benchmarks:
+ *   warps_per_column: 4 when the batch fills the GPU (4 column groups per SM);
+ *                     8 when it has at most 2 columns per SM (e.g. one 1024x440
+ *                     frame): the per-column critical path then sets the frame
+ *                     latency (BASELINE configs[1]; P:283-287 report per-frame
+ *                     rates), so each column gets twice the warps;
+ *   cols_per_cta    : column groups per CTA of that launch.
+ * Either pointer may be NULL.  Both are 0 before the first launch.
+ * Errors: ARG (h NULL). */
+int stixels_query_launch(const stixels_handle* h, int* warps_per_column, int* cols_per_cta);
+
+/* Launch plan of the DP kernel for the following calls: 0 = automatic (the
+ * default: 8 warps per column when a batch has at most 2 columns per SM, else
+ * 4), 4 or 8 = forced (tests cover both plans on every shape; 8 on a full batch
+ * is correct but slower).  Errors: ARG (h NULL or another value), UNSUPPORTED
+ * (8 when the column's shared memory does not allow it). */
+int stixels_set_launch_plan(stixels_handle* h, int warps_per_column);
+
 /* Synchronise and free everything the handle owns.  NULL is a no-op. */
 int stixels_destroy(stixels_handle* h);
 

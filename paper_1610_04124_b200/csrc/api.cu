@@ -25,6 +25,9 @@ struct stixels_handle {
   int W = 0, H = 0, max_batch = 0, device = 0;
   cudaStream_t stream = nullptr;
   int n_cols = 0, cap = 0, dp_slots = 128, cols_per_cta = 0, smem = 0, grid = 0, sms = 0;
+  int col_bytes8 = 0, cols_per_cta8 = 0;   // CW = 8 column groups (small batches), 0 = off
+  int last_cw = 0, last_cpc = 0;            // warps per column, groups per CTA of the last DP launch
+  int plan_cw = 0;                          // stixels_set_launch_plan: 0 auto, 4 or 8
   bool sparse = true;
   bool pair2d = false;          // NEXT f2: sigma_O(f) table given
   bool iw = false;              // int32 W-rows with atomic band rounds (band <= 3, exact mode)
@@ -40,8 +43,8 @@ struct stixels_handle {
   uint32_t* d_thr = nullptr;
   int* d_overflow = nullptr;
   float* d_scratch = nullptr;   // per-column-slot DP scratch of h->stream (and hs[0])
+  uint16_t* d_cols = nullptr;   // reduced columns of the two-launch plan [max_batch][n_cols][H]
   size_t scratch_bytes = 0;
-  uint16_t* d_cols = nullptr;
   // host-buffer path (lazily allocated): two stage streams, each with its own DP
   // scratch (hs[0] shares d_scratch with h->stream, which it waits for; hs[1] has
   // hscratch1), so DP launches of consecutive stages may overlap on the SMs
@@ -59,6 +62,36 @@ struct stixels_handle {
   int sticky = 0;
   int launches = 0;
 };
+
+
+// The DP kernel instantiation for the handle's model (f2 tables, sparse / dense
+// band, int32 atomic bands) and column-group width cw; `go(kernel)` launches it.
+template <int CW, typename Go>
+static void dispatch_dp_cw(const stixels_handle* h, Go&& go) {
+  if (h->dp_slots == 128) {
+    if (h->pair2d && h->sparse) go(dp_kernel<128, true, true, false, CW>);
+    else if (h->pair2d) go(dp_kernel<128, false, true, false, CW>);
+    else if (h->iw) go(dp_kernel<128, true, false, true, CW>);
+    else if (h->sparse) go(dp_kernel<128, true, false, false, CW>);
+    else go(dp_kernel<128, false, false, false, CW>);
+  } else {
+    if (h->pair2d && h->sparse) go(dp_kernel<256, true, true, false, CW>);
+    else if (h->pair2d) go(dp_kernel<256, false, true, false, CW>);
+    else if (h->iw) go(dp_kernel<256, true, false, true, CW>);
+    else if (h->sparse) go(dp_kernel<256, true, false, false, CW>);
+    else go(dp_kernel<256, false, false, false, CW>);
+  }
+}
+template <typename Go>
+static void dispatch_dp(const stixels_handle* h, int cw, Go&& go) {
+  if (cw == 8) dispatch_dp_cw<8>(h, go);
+  else dispatch_dp_cw<kCW>(h, go);
+}
+static const void* dp_kernel_ptr(const stixels_handle* h, int cw) {
+  const void* f = nullptr;
+  dispatch_dp(h, cw, [&](auto k) { f = (const void*)k; });
+  return f;
+}
 
 static thread_local std::string g_create_err;
 
@@ -229,7 +262,7 @@ const char* stixels_last_error(const stixels_handle* h) {
 
 static void free_all(stixels_handle* h) {
   cudaFree(h->d_E); cudaFree(h->d_E2); cudaFree(h->d_WT); cudaFree(h->d_M2); cudaFree(h->d_gG); cudaFree(h->d_gS);
-  cudaFree(h->d_dgR); cudaFree(h->d_thr); cudaFree(h->d_overflow); cudaFree(h->d_cols); cudaFree(h->d_scratch);
+  cudaFree(h->d_dgR); cudaFree(h->d_thr); cudaFree(h->d_overflow); cudaFree(h->d_scratch); cudaFree(h->d_cols);
   cudaFree(h->hscratch1);
   if (h->ev_entry) cudaEventDestroy(h->ev_entry);
   for (int i = 0; i < 2; ++i) {
@@ -437,17 +470,15 @@ int stixels_create(const stixels_params* params, int width, int height, int max_
   if (prop.major != 10) return bail(STIXELS_ERR_CUDA, "this library is built for sm_100a (B200) only");
   h->sms = prop.multiProcessorCount;
   int optin = (int)prop.sharedMemPerBlockOptin;
-  auto kfun = [&]() -> const void* {
-    if (DPv == 128)
-      return pair2d ? (sparse ? (const void*)dp_kernel<128, true, true> : (const void*)dp_kernel<128, false, true>)
-             : iw   ? (const void*)dp_kernel<128, true, false, true>
-             : sparse ? (const void*)dp_kernel<128, true, false> : (const void*)dp_kernel<128, false, false>;
-    return pair2d ? (sparse ? (const void*)dp_kernel<256, true, true> : (const void*)dp_kernel<256, false, true>)
-           : iw   ? (const void*)dp_kernel<256, true, false, true>
-           : sparse ? (const void*)dp_kernel<256, true, false> : (const void*)dp_kernel<256, false, false>;
-  };
-  int cb = DPv == 128 ? (sparse ? col_smem_bytes<128, true>(height) : col_smem_bytes<128, false>(height))
+  auto kfun = [&](int cw) { return dp_kernel_ptr(h, cw); };
+  auto cbytes = [&](int cw) {
+    if (cw == 8)
+      return DPv == 128 ? (sparse ? col_smem_bytes<128, true, 8>(height) : col_smem_bytes<128, false, 8>(height))
+                        : (sparse ? col_smem_bytes<256, true, 8>(height) : col_smem_bytes<256, false, 8>(height));
+    return DPv == 128 ? (sparse ? col_smem_bytes<128, true>(height) : col_smem_bytes<128, false>(height))
                       : (sparse ? col_smem_bytes<256, true>(height) : col_smem_bytes<256, false>(height));
+  };
+  int cb = cbytes(4);
   int sb = stx::kM2Pad + al16((height + 1) * 4) + (sparse ? stx::e_copies<true>() : stx::e_copies<false>()) * esz * 4 +
            al16(kTri * 2) +   // pad, M2, E copies, triangle decode
            (pair2d && sparse ? (DPv + 17) * 16 * 4 : 0) +  // NEXT f2 band weights
@@ -457,12 +488,23 @@ int stixels_create(const stixels_params* params, int width, int height, int max_
   h->cols_per_cta = cpc;
   h->smem = sb + cpc * cb;
   A.col_bytes = cb; A.shared_bytes = sb; A.cols_per_cta = cpc;
-  e = cudaFuncSetAttribute(kfun(), cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem);
+  e = cudaFuncSetAttribute(kfun(4), cudaFuncAttributeMaxDynamicSharedMemorySize, h->smem);
   if (e != cudaSuccess) return bail(STIXELS_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
   int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfun(), cpc * kCW * 32, h->smem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfun(4), cpc * kCW * 32, h->smem);
   if (e != cudaSuccess || per_sm < 1) return bail(STIXELS_ERR_UNSUPPORTED, "dp_kernel does not fit on an SM");
   h->grid = h->sms * per_sm;
+  // CW = 8 groups for batches of at most 2 columns per SM (latency): up to 2 per CTA,
+  // within the scratch slots of the CW = 4 plan
+  {
+    const int cb8 = cbytes(8);
+    const int cpc8 = std::min({2, cpc, (optin - sb) / cb8});
+    if (cpc8 >= 1 && per_sm == 1 &&
+        cudaFuncSetAttribute(kfun(8), cudaFuncAttributeMaxDynamicSharedMemorySize, sb + cpc8 * cb8) == cudaSuccess) {
+      h->col_bytes8 = cb8;
+      h->cols_per_cta8 = cpc8;
+    }
+  }
   // reduction tile
   const int in_bpp = bytes_per_px(params->disp_format);
   h->red_tc = std::max(1, std::min(h->n_cols, (in_bpp == 4 ? 256 : 512) / params->stixel_width));
@@ -505,7 +547,7 @@ int stixels_create(const stixels_params* params, int width, int height, int max_
 }
 
 #ifdef STX_TRACE
-// diagnostic build only: device buffer of 4*64*16 u64 for the phase timeline
+// diagnostic build only: device buffer of 4*64*32 u64 for the phase timeline
 extern "C" int stixels_trace_buffer(stixels_handle* h, void* d_buf) {
   if (!h) return STIXELS_ERR_ARG;
   h->args.trace = (unsigned long long*)d_buf;
@@ -543,6 +585,26 @@ static int launch_reduce(stixels_handle* h, const void* d_disp, int64_t pitch, i
   r.out = d_cols;
   dim3 grid((h->n_cols + h->red_tc - 1) / h->red_tc, (h->H + kRedRows - 1) / kRedRows, batch);
   const bool med = h->p.reduce_mode == STIXELS_REDUCE_MEDIAN;
+  // row-wise register kernel for the common widths (16-byte aligned frames)
+  if (r.vec && (r.s == 3 || r.s == 5 || r.s == 7 || r.s == 10)) {
+    auto go_rr = [&](auto kern, int G) {
+      const int ngroups = (h->n_cols + G - 1) / G;
+      dim3 g((ngroups + kRRWarps - 1) / kRRWarps, (h->H + 31) / 32, batch);
+      kern<<<g, 32 * kRRWarps, 0, s>>>(r);
+    };
+#define STX_RR(BPPV, SWV)                                                                        \
+    if (r.bpp == BPPV && r.s == SWV) {                                                            \
+      if (med) go_rr(reduce_rows_kernel<true, BPPV, SWV>, RowRed<BPPV, SWV>::G);                  \
+      else go_rr(reduce_rows_kernel<false, BPPV, SWV>, RowRed<BPPV, SWV>::G);                     \
+    }
+    STX_RR(2, 5) else STX_RR(2, 3) else STX_RR(2, 7) else STX_RR(2, 10)
+    else STX_RR(1, 5) else STX_RR(1, 3) else STX_RR(1, 7) else STX_RR(1, 10)
+    else STX_RR(4, 5) else STX_RR(4, 3) else STX_RR(4, 7) else STX_RR(4, 10)
+#undef STX_RR
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(h, STIXELS_ERR_CUDA, std::string("reduce_rows_kernel: ") + cudaGetErrorString(e));
+    return STIXELS_OK;
+  }
   const bool s5 = r.s == 5;                          // the headline width, compile-time
   auto go = [&](auto kern) { kern<<<grid, kRedThreads, h->red_smem, s>>>(r); };
   if (r.bpp == 4) {
@@ -558,6 +620,14 @@ static int launch_reduce(stixels_handle* h, const void* d_disp, int64_t pitch, i
   return STIXELS_OK;
 }
 
+// Warps per column of the DP launch for `batch` frames: 8 (latency plan) when the
+// batch has at most cols_per_cta8 columns per SM, else 4; or the forced plan.
+static int plan_cw(const stixels_handle* h, int batch) {
+  if (h->plan_cw) return h->plan_cw;
+  const long need = ((long)batch * h->n_cols + h->sms - 1) / h->sms;
+  return (h->cols_per_cta8 > 0 && need <= h->cols_per_cta8) ? 8 : kCW;
+}
+
 static int launch_dp(stixels_handle* h, const uint16_t* d_cols, int batch, stixel_t* d_out,
                      int32_t* d_count, float* d_cost, cudaStream_t s, float* scratch) {
   DPArgs A = h->args;
@@ -566,27 +636,22 @@ static int launch_dp(stixels_handle* h, const uint16_t* d_cols, int batch, stixe
   A.items = batch * h->n_cols;
   // Column groups per CTA: the full count when the batch fills the GPU; fewer when
   // it does not (e.g. one frame: 204 columns for 148 SMs), so the columns spread
-  // over more SMs instead of sharing a few (latency, BASELINE configs[1]).
-  const int C = std::max(1, std::min(h->cols_per_cta, (A.items + h->sms - 1) / h->sms));
+  // over more SMs instead of sharing a few; and then 8 warps per column (CW = 8),
+  // which shortens the per-column critical path (latency, BASELINE configs[1]).
+  const int need = (A.items + h->sms - 1) / h->sms;     // columns per SM
+  const int cw = plan_cw(h, batch);
+  const int C = std::max(1, std::min(cw == 8 ? h->cols_per_cta8 : h->cols_per_cta, need));
   A.cols_per_cta = C;
+  if (cw == 8) A.col_bytes = h->col_bytes8;
   const int smem = A.shared_bytes + C * A.col_bytes;
   int grid = std::min(h->grid, (A.items + C - 1) / C);
-  const int threads = C * kCW * 32;
-  if (h->dp_slots == 128) {
-    if (h->pair2d && h->sparse) dp_kernel<128, true, true><<<grid, threads, smem, s>>>(A);
-    else if (h->pair2d) dp_kernel<128, false, true><<<grid, threads, smem, s>>>(A);
-    else if (h->iw) dp_kernel<128, true, false, true><<<grid, threads, smem, s>>>(A);
-    else if (h->sparse) dp_kernel<128, true, false><<<grid, threads, smem, s>>>(A);
-    else dp_kernel<128, false, false><<<grid, threads, smem, s>>>(A);
-  } else {
-    if (h->pair2d && h->sparse) dp_kernel<256, true, true><<<grid, threads, smem, s>>>(A);
-    else if (h->pair2d) dp_kernel<256, false, true><<<grid, threads, smem, s>>>(A);
-    else if (h->iw) dp_kernel<256, true, false, true><<<grid, threads, smem, s>>>(A);
-    else if (h->sparse) dp_kernel<256, true, false><<<grid, threads, smem, s>>>(A);
-    else dp_kernel<256, false, false><<<grid, threads, smem, s>>>(A);
-  }
+  const int threads = C * cw * 32;
+  auto go = [&](auto kern) { kern<<<grid, threads, smem, s>>>(A); };
+  dispatch_dp(h, cw, go);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(h, STIXELS_ERR_CUDA, std::string("dp_kernel: ") + cudaGetErrorString(e));
+  h->last_cw = cw;
+  h->last_cpc = C;
   return STIXELS_OK;
 }
 
@@ -659,8 +724,8 @@ int stixels_compute_host(stixels_handle* h, const void* h_disp, int64_t pitch, i
     for (int i = 0; i < 2; ++i) {
       cudaFree(h->hin[i]); cudaFree(h->hout[i]); cudaFree(h->hcnt[i]); cudaFree(h->hcost[i]);
       cudaFree(h->hcols[i]);
-      h->hin[i] = nullptr; h->hout[i] = nullptr; h->hcnt[i] = nullptr; h->hcost[i] = nullptr;
       h->hcols[i] = nullptr;
+      h->hin[i] = nullptr; h->hout[i] = nullptr; h->hcnt[i] = nullptr; h->hcost[i] = nullptr;
       if (!h->hs[i]) CU(cudaStreamCreateWithFlags(&h->hs[i], cudaStreamNonBlocking), h);
       CU(cudaMalloc(&h->hin[i], in_b * chunk), h);
       CU(cudaMalloc(&h->hout[i], sizeof(stixel_t) * (size_t)chunk * h->n_cols * h->cap), h);
@@ -720,6 +785,22 @@ int stixels_sync(stixels_handle* h) {
 }
 
 int stixels_last_launch_count(const stixels_handle* h) { return h ? h->launches : 0; }
+
+int stixels_set_launch_plan(stixels_handle* h, int warps_per_column) {
+  if (!h || (warps_per_column != 0 && warps_per_column != 4 && warps_per_column != 8))
+    return STIXELS_ERR_ARG;
+  if (warps_per_column == 8 && h->cols_per_cta8 < 1)
+    return fail(h, STIXELS_ERR_UNSUPPORTED, "8 warps per column: shared memory too small for this shape");
+  h->plan_cw = warps_per_column;
+  return STIXELS_OK;
+}
+
+int stixels_query_launch(const stixels_handle* h, int* warps_per_column, int* cols_per_cta) {
+  if (!h) return STIXELS_ERR_ARG;
+  if (warps_per_column) *warps_per_column = h->last_cw;
+  if (cols_per_cta) *cols_per_cta = h->last_cpc;
+  return STIXELS_OK;
+}
 
 int stixels_destroy(stixels_handle* h) {
   if (!h) return STIXELS_OK;

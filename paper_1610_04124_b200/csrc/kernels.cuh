@@ -188,6 +188,119 @@ __global__ void __launch_bounds__(kRedThreads) reduce_kernel(ReduceArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// K1 (row-wise variant, the default when its span fits): lanes own consecutive
+// image rows, each thread G = 16 / gcd(16, s bpp) consecutive reduced columns of
+// its row, so its bytes start 16-byte aligned and are NV = G s bpp / 16 vector
+// loads straight into registers (no shared-memory tile); the pixels are unpacked
+// at compile-time offsets.  A warp reads 32 rows x NV x 16 bytes (the 32-byte
+// sectors shared by neighbouring spans are L1 hits) and writes, per column, 32
+// consecutive model rows (64 bytes, coalesced).  Same arithmetic as reduce_kernel
+// (decode and validity L#23/L#28, mean P:195 or median L#24, half-up rounding to
+// 1/256, the L#27 clamp); the rounding division is a multiply-high by a per-CTA
+// table floor(2^32 / d) and one correction step.
+// ---------------------------------------------------------------------------
+__host__ __device__ constexpr int rr_gcd(int x, int y) { return y == 0 ? x : rr_gcd(y, x % y); }
+template <int BPP, int SW>
+struct RowRed {
+  static constexpr int G = 16 / rr_gcd(16, SW * BPP);    // reduced columns per thread
+  static constexpr int NV = G * SW * BPP / 16;           // 16-byte loads per thread
+};
+constexpr int kRRWarps = 8;                              // warps (column groups) per CTA
+
+template <bool MEDIAN, int BPP, int SW>
+__global__ void __launch_bounds__(32 * kRRWarps) reduce_rows_kernel(ReduceArgs a) {
+  using RR = RowRed<BPP, SW>;
+  constexpr int G = RR::G, NV = RR::NV;
+  __shared__ uint32_t rcp[2 * SW + 2];
+  for (int i = threadIdx.x; i < 2 * SW + 2; i += blockDim.x)
+    rcp[i] = i < 2 ? 0u : (uint32_t)((1ull << 32) / (unsigned)i);
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int cg = blockIdx.x * kRRWarps + (threadIdx.x >> 5);      // column group
+  const int r = blockIdx.y * 32 + lane;                           // image row
+  const int frame = blockIdx.z;
+  const int c0 = cg * G;
+  if (c0 >= a.n_cols || r >= a.H) return;
+  const int64_t sb = (int64_t)c0 * SW * BPP;                      // span start (16-byte aligned)
+  const uint8_t* row = a.disp + ((int64_t)frame * a.H + r) * a.pitch;
+  uint32_t wv[NV * 4];
+  if (sb + NV * 16 <= a.pitch) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const uint4 x = __ldg(reinterpret_cast<const uint4*>(row + sb) + i);
+      wv[4 * i] = x.x; wv[4 * i + 1] = x.y; wv[4 * i + 2] = x.z; wv[4 * i + 3] = x.w;
+    }
+  } else {
+    // the last group of a tight row: element loads within [0, W bpp)
+#pragma unroll
+    for (int i = 0; i < NV * 4; ++i) wv[i] = 0u;
+    const int lim_b = a.W * BPP - (int)sb;
+#pragma unroll
+    for (int e = 0; e < NV * 16 / BPP; ++e) {
+      if (e * BPP < lim_b) {
+        uint32_t x;
+        if constexpr (BPP == 4) x = __ldg(reinterpret_cast<const uint32_t*>(row + sb) + e);
+        else if constexpr (BPP == 2) x = __ldg(reinterpret_cast<const uint16_t*>(row + sb) + e);
+        else x = __ldg(row + sb + e);
+        wv[(e * BPP) >> 2] |= x << (8 * ((e * BPP) & 3));
+      }
+    }
+  }
+  const uint32_t lim = (uint32_t)a.D << a.q_bits;
+  const int shift = kRBits + 1 - a.q_bits;
+  const float Df = (float)a.D;
+  const int v = a.H - 1 - r;
+  uint16_t* out = a.out + ((int64_t)frame * a.n_cols + c0) * a.H + v;
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    if (c0 + g >= a.n_cols) break;
+    uint32_t u[SW];
+    bool ok[SW];
+    uint32_t sum = 0, n = 0;
+#pragma unroll
+    for (int x = 0; x < SW; ++x) {
+      const int e = g * SW + x;                          // pixel index in the span
+      const uint32_t w = wv[(e * BPP) >> 2];
+      if constexpr (BPP == 4) {
+        const float d = __uint_as_float(w);
+        ok[x] = d >= 0.f && d < Df;                      // false for NaN and +-inf too
+        u[x] = ok[x] ? (uint32_t)__float2int_rd(d * 256.f + 0.5f) : 0u;   // L#28
+      } else {
+        u[x] = BPP == 2 ? ((w >> (8 * ((e * 2) & 3))) & 0xffffu) : ((w >> (8 * (e & 3))) & 0xffu);
+        ok[x] = (u[x] != a.invalid) && (u[x] < lim);
+      }
+      sum += ok[x] ? u[x] : 0u;
+      n += ok[x] ? 1u : 0u;
+    }
+    if (MEDIAN && n) {
+      const uint32_t k1 = (n - 1) >> 1, k2 = n >> 1;
+      uint32_t va = 0, vb = 0;
+#pragma unroll
+      for (int x = 0; x < SW; ++x) {
+        uint32_t less = 0, leq = 0;
+#pragma unroll
+        for (int y = 0; y < SW; ++y) {
+          less += (ok[y] && u[y] < u[x]) ? 1u : 0u;
+          leq += (ok[y] && u[y] <= u[x]) ? 1u : 0u;
+        }
+        if (ok[x] && less <= k1 && k1 < leq) va = u[x];
+        if (ok[x] && less <= k2 && k2 < leq) vb = u[x];
+      }
+      sum = va + vb;
+      n = 2;
+    }
+    uint16_t val = 0xFFFF;
+    if (n) {
+      const uint32_t num = (sum << shift) + n, d = 2u * n;   // num < 2^32: sum < SW 2^16
+      uint32_t q = __umulhi(num, rcp[d]);
+      if (num - q * d >= d) ++q;                          // floor(2^32/d) under-estimates by <= 1
+      val = (uint16_t)min(q, ((uint32_t)(a.D - 1) << kRBits) + (1u << (kRBits - 1)) - 1u);
+    }
+    out[(int64_t)g * a.H] = val;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // K3: DP kernel (prefix sums + object-LUT rows + Eq. 5-6 DP + backtracking).
 //
 // Work unit: one column, handled by a "column group" of kCW = 4 warps with its
@@ -241,7 +354,7 @@ __device__ __forceinline__ unsigned long long stx_globaltimer() {
 #define STX_STAMP(blk, slot)                                                             \
   do {                                                                                   \
     if (blockIdx.x == 0 && first_item && lane == 0 && (blk) < 64)                        \
-      a.trace[(cslot * 64 + (blk)) * 16 + (slot)] = stx_globaltimer();                  \
+      a.trace[(cslot * 64 + (blk)) * 32 + (slot)] = stx_globaltimer();                  \
   } while (0)
 #else
 #define STX_STAMP(blk, slot) do { } while (0)
@@ -278,13 +391,14 @@ struct DPArgs {
   const float* WTg;        // NEXT f2: [DP+17][16] band weights cap - Pair[d+o-7][d] at row d+1
   int gG_stride;
 #ifdef STX_TRACE
-  unsigned long long* trace;     // diagnostic build only: [4 groups][64 blocks][16] clock64 stamps
+  unsigned long long* trace;     // diagnostic build only: [4 groups][64 blocks][32] globaltimer stamps
 #endif
 };
 
 struct ColSmem {
   float* priv;      // [32][DP+1]     priv[i][f] = LUT_object[f][32b+i+1] of the block being built
-  float* seed;      // [2][DP] W-row 32b+16 of block b (slot b & 1)
+  float* seed;      // [2][NSEED][DP] W-rows 32b+8i (i >= 1) of block b (slot b & 1): the
+                    // newest chunk's seeds (NSEED = 1 for CW = 4, 3 for CW = 8)
   float* ring;      // [4][ring_stride] per-warp W-rows W_j = LUT_object[.][j] - cap*j (RR = 2 sparse, 4 dense)
   float4* cell;     // [496]          triangle cells (bottom K0+1+j', target K0+k' > j'), one
                     //                16-byte record each (one LDS.128 in the serial chain):
@@ -330,18 +444,24 @@ __host__ __device__ constexpr int priv_stride() { return DP + 3; }
 template <bool SPARSE>
 __host__ __device__ constexpr int e_copies() { return SPARSE ? 1 : 4; }
 
-template <int DP, bool SPARSE>
+// Warps sharing the newest chunk (the 32 bottoms of the block just finalised):
+// 2 x 16 rows with 4 warps per column, 4 x 8 rows with 8 (latency plan).
+__host__ __device__ constexpr int newest_warps(int cw) { return cw == 8 ? 4 : 2; }
+// Triangle-cell buffers: the latency plan (CW = 8) precomputes block b+1's cells
+// while the serial warp still reads block b's, so it double-buffers them.
+__host__ __device__ constexpr int cell_bufs(int cw) { return cw == 8 ? 2 : 1; }
+template <int DP, bool SPARSE, int CW = kCW>
 __host__ __device__ inline int col_smem_bytes(int h) {
   int b = 0;
   b += al16(32 * priv_stride<DP>() * 4);
-  b += al16(2 * DP * 4);
-  b += al16(kCW * ring_stride<DP, SPARSE>() * 4);
-  b += kTri * 16;
+  b += al16((2 * newest_warps(CW) - 2) * DP * 4);
+  b += al16(CW * ring_stride<DP, SPARSE>() * 4);
+  b += kTri * 16 * cell_bufs(CW);
   b += al16((h + 3) * 32);
   b += al16((h + 2) * 4);
   b += al16(h * 2) * 3;
   b += al16(h);
-  b += al16(kCW * 32 * 8);
+  b += al16(CW * 32 * 8);
   b += al16(32 * 16);
   b += 16;
   return b;
@@ -352,20 +472,20 @@ __host__ __device__ inline int64_t col_scratch_floats(int h) {
   return 2 * (int64_t)(h + 1) + (int64_t)(((h + 31) >> 5) + 1) * DP;
 }
 
-template <int DP, bool SPARSE>
+template <int DP, bool SPARSE, int CW>
 __device__ inline ColSmem carve(uint8_t* p, int h) {
   ColSmem w;
   w.priv = reinterpret_cast<float*>(p); p += al16(32 * priv_stride<DP>() * 4);
-  w.seed = reinterpret_cast<float*>(p); p += al16(2 * DP * 4);
-  w.ring = reinterpret_cast<float*>(p); p += al16(kCW * ring_stride<DP, SPARSE>() * 4);
-  w.cell = reinterpret_cast<float4*>(p); p += kTri * 16;
+  w.seed = reinterpret_cast<float*>(p); p += al16((2 * newest_warps(CW) - 2) * DP * 4);
+  w.ring = reinterpret_cast<float*>(p); p += al16(CW * ring_stride<DP, SPARSE>() * 4);
+  w.cell = reinterpret_cast<float4*>(p); p += kTri * 16 * cell_bufs(CW);
   w.rec = reinterpret_cast<uint4*>(p); p += al16((h + 3) * 32);
   w.eo = reinterpret_cast<uint32_t*>(p); p += al16((h + 2) * 4);
   w.argO = reinterpret_cast<uint16_t*>(p); p += al16(h * 2);
   w.argG = reinterpret_cast<uint16_t*>(p); p += al16(h * 2);
   w.argS = reinterpret_cast<uint16_t*>(p); p += al16(h * 2);
   w.fpv = p; p += al16(h);
-  w.part = reinterpret_cast<float2*>(p); p += al16(kCW * 32 * 8);
+  w.part = reinterpret_cast<float2*>(p); p += al16(CW * 32 * 8);
   w.pgps = reinterpret_cast<float4*>(p); p += al16(32 * 16);
   w.ctr = reinterpret_cast<int*>(p);
   return w;
@@ -485,7 +605,10 @@ __host__ __device__ constexpr int wt_rows() { return DP + 17; }   // drp 0 .. no
 // shared-memory integer atomics on 8-lane groups (float atomics would be CAS
 // loops).  Exact: every W entry is an integer number of quanta below 2^24 (L#22),
 // so the order of the adds does not matter and the gathers convert exactly.
-template <int DP, bool SPARSE, bool PAIR2D, bool IW = false>
+// CW: warps per column group -- kCW = 4 (4 groups per CTA) when the batch fills the
+// GPU; 8 (at most 2 groups per CTA) for small batches, where the per-column
+// critical path (the frame latency, BASELINE configs[1]) rather than throughput binds.
+template <int DP, bool SPARSE, bool PAIR2D, bool IW = false, int CW = kCW>
 __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_constant__ DPArgs a) {
   constexpr int NR = DP / 128;         // LDS.128 ring windows per lane
   constexpr int NS = DP / 32;          // 32-wide f slices
@@ -497,9 +620,9 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
   // that a column's warps sit on different SM sub-partitions where possible.
   const int C = a.cols_per_cta;
   int cslot, w;
-  if (wid >= 3 * C) {
-    cslot = wid - 3 * C; w = 0;
-  } else if (C == 4) {
+  if (wid >= (CW - 1) * C) {
+    cslot = wid - (CW - 1) * C; w = 0;
+  } else if (CW == 4 && C == 4) {
     cslot = ((wid & 3) + (wid >> 2) + 1) & 3; w = 1 + (wid >> 2);
   } else {
     cslot = wid % C; w = 1 + wid / C;
@@ -515,7 +638,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
   const int capI = IW ? __float2int_rn(capQ) * kIWS : 0;
   const int goHiI = toI(a.kGO_hi), goLoI = toI(a.kGO_lo), goMidI = toI(a.kGO_mid);
   const int bar_col = 1 + cslot;       // 128 threads: whole column group
-  const int bar_rect = 1 + C + cslot;  // 96 threads: rectangle warps
+  const int bar_rect = 1 + C + cslot;  // (CW - 1) * 32 threads: rectangle warps
   const int bar_x = 1 + 2 * C + cslot; // 96 arrive + 32 sync: next block's priv rows ready
 
   // CTA-shared tables: M2 at offset 0, then 4 shifted copies of the object
@@ -545,9 +668,11 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
   __syncthreads();
   const uint8_t* Eb = reinterpret_cast<const uint8_t*>(E);
 
-  ColSmem cs = carve<DP, SPARSE>(smem + a.shared_bytes + cslot * a.col_bytes, h);
+  ColSmem cs = carve<DP, SPARSE, CW>(smem + a.shared_bytes + cslot * a.col_bytes, h);
   // {T[j], N4[j]} of row j: the first 8 bytes of the record's second half
   auto tn_at = [&](int j) { return *reinterpret_cast<const uint2*>(cs.rec + 2 * j + 1); };
+  // triangle cells of block bt (double-buffered in the latency plan)
+  auto cells_of = [&](int bt) { return cs.cell + (cell_bufs(CW) == 2 ? (bt & 1) * kTri : 0); };
   float* ringw = cs.ring + w * ring_stride<DP, SPARSE>();
   const float INF = __int_as_float(0x7f800000);
   const int slot_global = blockIdx.x * a.cols_per_cta + cslot;
@@ -797,18 +922,13 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
   (void)first_item;
   for (int item = slot_global; item < a.items; item += gridDim.x * a.cols_per_cta) {
     const uint16_t* col = a.cols + (int64_t)item * h;
+    if (w == 0) STX_STAMP(60, 0);       // item start
     // ---------------- prologue A (all 4 warps): per-pixel costs (a3-a4) ----------
     float* tG = cs.priv;                 // temporaries in the (idle) priv rows
     float* tS = cs.priv + h;
     uint32_t* tD = reinterpret_cast<uint32_t*>(cs.priv + 2 * h);
-    for (int v = ctid; v < h + 2; v += kCW * 32) {
-      int dR = -1;
-      if (v < h) {
-        uint32_t u = col[v];
-        // (clamped below D - 1/2 as stixels_reduce does, L#27, so caller-made
-        // columns cannot push an object mean past the table)
-        dR = (u == 0xffffu) ? -1 : min((int)u, ((a.D - 1) << kRBits) + (1 << (kRBits - 1)) - 1);
-      }
+    // one row v of prologue A from its reduced value dR (-1 invalid)
+    auto prologue_row = [&](int v, int dR) {
       const bool valid = dR >= 0;
       const int dr = valid ? (dR + (1 << (kRBits - 1))) >> kRBits : -1;   // round half up (L#9)
       if (v < h) {
@@ -835,10 +955,21 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
       // (PAIR2D) the row index d of the 2-D table (D + 1 = invalid)
       const uint32_t ehi = PAIR2D ? (uint32_t)(valid ? dr : a.D + 1) : (uint32_t)(dmr * 4);
       cs.eo[v] = (uint32_t)(cc * a.esz * 4 + (dmr - cc) * 4) | (ehi << 16);
+    };
+    for (int v = ctid; v < h + 2; v += CW * 32) {
+      int dR = -1;
+      if (v < h) {
+        uint32_t u = col[v];
+        // (clamped below D - 1/2 as stixels_reduce does, L#27, so caller-made
+        // columns cannot push an object mean past the table)
+        dR = (u == 0xffffu) ? -1 : min((int)u, ((a.D - 1) << kRBits) + (1 << (kRBits - 1)) - 1);
+      }
+      prologue_row(v, dR);
     }
-    for (int i = ctid; i < DP; i += kCW * 32) ANg[i] = 0.f;   // W[.][0] = 0
+
+    for (int i = ctid; i < DP; i += CW * 32) ANg[i] = 0.f;   // W[.][0] = 0
     if (ctid == 0) *cs.ctr = 0;
-    named_bar(bar_col, kCW * 32);
+    named_bar(bar_col, CW * 32);
     STX_STAMP(63, w);                    // clock calibration (all warps just released)
 
     // ---------------- prologue B (4 warps): prefix sums --------------
@@ -847,7 +978,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
       float cf = 0.f;
       uint32_t cu = 0;
       if (lane == 0) { if (w == 0) PGg[0] = 0.f; if (w == 1) PSg[0] = 0.f; }
-      for (int v0 = 0; v0 < h; v0 += 32) {
+      for (int v0 = 0; v0 < (w < 4 ? h : 0); v0 += 32) {     // warps 4.. (CW = 8) idle
         const int v = v0 + lane;
         if (w < 2) {
           const float x = (v < h) ? ((w == 0) ? tG[v] : tS[v]) : 0.f;
@@ -867,7 +998,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
       }
       __threadfence_block();
     }
-    named_bar(bar_col, kCW * 32);
+    named_bar(bar_col, CW * 32);
 
     // build priv W-rows of block bt and the anchor row 32(bt+1): a sequential
     // prefix over rows, per f, so the f slices are independent.  Two
@@ -934,7 +1065,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
         // Cell = {data x 32 | code, min(data + gravity prior, BIG) x 32 | code, f,
         // f - ord_margin}, code = j' + 1 (the bottom's place in the block, L#17).
         const int* pv = reinterpret_cast<const int*>(cs.priv);
-        int4* cl = reinterpret_cast<int4*>(cs.cell);
+        int4* cl = reinterpret_cast<int4*>(cells_of(bt));
         const int wq = t0 >> 5, nq = nthr >> 5;       // this warp's index among nq warps
         for (int it = wq; it < 16; it += nq) {
           const bool lo = lane < 31 - it;
@@ -966,17 +1097,22 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
           const int jr = K0b + jp + 1;
           const int2 th = thrS[jr];
           const float pen = (f >= th.x) ? a.kGO_hi : ((f < th.y) ? a.kGO_lo : a.kGO_mid);
-          cs.cell[idx] = make_float4(data, data + pen, __int_as_float(f), 0.f);
+          cells_of(bt)[idx] = make_float4(data, data + pen, __int_as_float(f), 0.f);
         }
       }
       }
     };
-    // seed of the second half of block bt's newest chunk: W-row K0 + 16 (priv row 15)
+    // seeds of block bt's newest chunk beyond its first part: W-rows K0 + 32 i / NWN
+    // (priv rows 32 i / NWN - 1), i = 1 .. NWN - 1
+    constexpr int NWN = newest_warps(CW);
     auto copy_seed = [&](int bt) {
       if ((bt << 5) + 32 < h) {          // only needed if a next block exists
-        float* sd = cs.seed + (bt & 1) * DP;
-        const float* row = cs.priv + 15 * priv_stride<DP>();
-        for (int f = lane; f < DP; f += 32) sd[f] = row[f];
+#pragma unroll
+        for (int i = 1; i < NWN; ++i) {
+          float* sd = cs.seed + ((bt & 1) * (NWN - 1) + i - 1) * DP;
+          const float* row = cs.priv + (32 / NWN * i - 1) * priv_stride<DP>();
+          for (int f = lane; f < DP; f += 32) sd[f] = row[f];
+        }
       }
     };
 
@@ -985,7 +1121,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
       for (int c = 0; c < NB; ++c) fr[c] = 0;
       build_priv(0);
     }
-    named_bar(bar_col, kCW * 32);
+    named_bar(bar_col, CW * 32);
 
     // block 0 has only the j = 0 candidate (Eq. 5) and its triangle
     {
@@ -1001,10 +1137,10 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
         rargj = 0;
       }
       cs.part[w * 32 + lane] = make_float2(rbest, __int_as_float(rargj));
-      precompute_cells(0, ctid, kCW * 32);
+      precompute_cells(0, ctid, CW * 32);
       if (w == 2) copy_seed(0);
     }
-    named_bar(bar_col, kCW * 32);
+    named_bar(bar_col, CW * 32);
 
     // serial-warp state carried across blocks (warp-uniform): last row's C values,
     // ground / sky running minima (value, argmin) of Eq. 6's G and S rows
@@ -1030,7 +1166,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
         float best = INF;
         int argj = 0x7fffffff;
 #pragma unroll
-        for (int q = 0; q < kCW; ++q) {
+        for (int q = 0; q < CW; ++q) {
           float2 p = cs.part[q * 32 + lane];
           int pj = __float_as_int(p.y);
           if (p.x < best || (p.x == best && pj < argj)) { best = p.x; argj = pj; }
@@ -1067,7 +1203,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
           pq[lane] = make_int2(toI(kOG - pg0), toI(pg1));
           __syncwarp();
           const int oh = toI(a.kOO_hi), ol = toI(a.kOO_lo);
-          const int4* cl = reinterpret_cast<const int4*>(cs.cell);
+          const int4* cl = reinterpret_cast<const int4*>(cells_of(b));
           int mgI = toI(mg);
           int prevCG = toI(__shfl_sync(0xffffffffu, pg1, 0) + mg);
           int bI = toI(best);
@@ -1077,7 +1213,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
           int rB = __shfl_sync(0xffffffffu, bI, 1);
           int rF = __shfl_sync(0xffffffffu, argf, 1);
           int off = 0;                                  // tri_off(jp)
-          STX_STAMP(b, 13);
+          STX_STAMP(b, 21);
           for (int jp = 0; jp < jn; ++jp) {
             const int2 q = pq[jp + 1];
             const int4 dcell = cl[off];                 // diagonal cell (bottom j, target j)
@@ -1085,6 +1221,14 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
             const bool take = dc < rB;
             const int COj = take ? dc : rB;
             const int Fj = take ? dcell.z : rF;
+            // latency plan: the next target's running minimum over bottoms < j comes
+            // from its lane BEFORE this step's update, and its cell at bottom j is
+            // evaluated here redundantly, so the shuffle leaves the loop-carried chain
+            int pB = 0, pF = 0;
+            if constexpr (CW == 8) {
+              pB = __shfl_sync(0xffffffffu, bI, (jp + 2) & 31);
+              pF = __shfl_sync(0xffffffffu, afI, (jp + 2) & 31);
+            }
             {
               const int4 lc = cl[off + lane - jp - 1];  // (lanes <= jp read a dead slot)
               const int cand = min(lc.x + prevCO + ((lc.w > prevF) ? oh : ol), lc.y + prevCG);
@@ -1092,8 +1236,16 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
               bI = upd ? cand : bI;
               afI = upd ? lc.z : afI;
             }
-            rB = __shfl_sync(0xffffffffu, bI, (jp + 2) & 31);
-            rF = __shfl_sync(0xffffffffu, afI, (jp + 2) & 31);
+            if constexpr (CW == 8) {
+              const int4 nc = cl[min(off + 1, kTri - 1)];  // cell (bottom j, target j + 1)
+              const int nd = min(nc.x + prevCO + ((nc.w > prevF) ? oh : ol), nc.y + prevCG);
+              const bool nt = nd < pB;                      // same rule as the lane's update
+              rB = nt ? nd : pB;
+              rF = nt ? nc.z : pF;
+            } else {
+              rB = __shfl_sync(0xffffffffu, bI, (jp + 2) & 31);
+              rF = __shfl_sync(0xffffffffu, afI, (jp + 2) & 31);
+            }
             mgI = min(mgI, prevCO + q.x);               // ground chain (value only)
             prevCG = q.y + mgI;
             prevCO = min(COj & ~31, kChainBig);
@@ -1115,14 +1267,14 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
         float rB = __shfl_sync(0xffffffffu, best, 1);
         int rF = __shfl_sync(0xffffffffu, argf, 1);
         int off = 0;                                    // tri_off(jp)
-        STX_STAMP(b, 13);                 // serial: merge + recovery + chain setup done
+        STX_STAMP(b, 21);                 // serial: merge + recovery + chain setup done
         for (int jp = 0; jp < jn; ++jp) {
           const int j = K0 + jp + 1;                    // bottom j; target j finalised
           const float4 q = cs.pgps[jp + 1];
           // diagonal cell (bottom j, target j), evaluated redundantly by all lanes
           // (data + min(aO, aG) computed as min(data + aO, (data + pen) + C_G): the
           // same value, exactly so in exact mode (integer quanta))
-          const float4 dcell = cs.cell[off];
+          const float4 dcell = cells_of(b)[off];
           const float dd = dcell.x;
           const float dg = dcell.y;
           const int df = __float_as_int(dcell.z);
@@ -1134,7 +1286,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
           // this lane's cell (bottom j, target k > j) with the same predecessors
           {
             const int idx = off + lane - jp - 1;        // (lanes <= jp read a dead slot)
-            const float4 lc = cs.cell[idx];
+            const float4 lc = cells_of(b)[idx];
             const float data = lc.x;
             const float dgl = lc.y;
             const int f = __float_as_int(lc.z);
@@ -1158,7 +1310,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
           off += 31 - jp;
         }
         }
-        STX_STAMP(b, 14);                 // serial: triangle chain done
+        STX_STAMP(b, 22);                 // serial: triangle chain done
         // ---- ground / sky argmins and values of the block's rows, as warp scans ----
         // lane l = row j = K0 + l = target k: candidates at bottom j use C[j-1]
         const float up_best = __shfl_up_sync(0xffffffffu, best, 1);     // all lanes shuffle
@@ -1198,7 +1350,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
           const float pG = __shfl_sync(0xffffffffu, CGk, src);
           const int pF = __shfl_sync(0xffffffffu, argf, src);
           if (tri_c) {
-            const int4 lc = reinterpret_cast<const int4*>(cs.cell)[tri_off(src) + lane - src - 1];
+            const int4 lc = reinterpret_cast<const int4*>(cells_of(b))[tri_off(src) + lane - src - 1];
             const int tO = lc.x + min(toI(pO), kChainBig) + ((lc.w > pF) ? toI(a.kOO_hi) : toI(a.kOO_lo));
             const int tG = lc.y + toI(pG);
             argc = (tG <= tO) ? 0 : 1;
@@ -1213,7 +1365,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
         if (K0 + 31 >= h - 1) {
           lastO = cCO; lastG = cCG; lastS = __shfl_sync(0xffffffffu, CSk, L);
         }
-        STX_STAMP(b, 15);                 // serial: scans + carries done
+        STX_STAMP(b, 23);                 // serial: scans + carries done
         // every lane now holds the final values of its target row k: write the
         // record of row k+1 (consumed by later rectangles; predecessor terms
         // shifted by -cap*(k+1)) and the index table
@@ -1235,12 +1387,12 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
           cs.fpv[k] = (uint8_t)argf;
         }
         STX_STAMP(b, 1);
-        if (has_next) named_bar(bar_x, kCW * 32);   // block b+1's priv rows are ready
+        if (has_next) named_bar(bar_x, CW * 32);   // block b+1's priv rows are ready
       } else if (has_next) {
         if (w == 1 || w == 2) build_priv(bn);   // block b's priv rows are no longer needed
         if (w == 1) STX_STAMP(b, 2);
-        named_bar(bar_rect, 3 * 32);
-        asm volatile("bar.arrive %0, %1;" ::"r"(bar_x), "r"(kCW * 32) : "memory");
+        named_bar(bar_rect, (CW - 1) * 32);
+        asm volatile("bar.arrive %0, %1;" ::"r"(bar_x), "r"(CW * 32) : "memory");
       }
       // ======== all warps: block b+1, bottoms final before block b ===============
       Acc acc;
@@ -1263,6 +1415,12 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
           acc.b1 = reinterpret_cast<const CT*>(pp1)[span_f(r1.x, r1.y, smem, Dm1)] / (IW ? kIWS : 1) + pf;
           acc.a0 = acc.a1 = 0;
         }
+        if (CW == 8 && w >= NWN) {
+          // latency plan: block b+1's triangle cells (into the other cell buffer)
+          // and newest-chunk seeds now, so the newest phase is the 4 x 8-row run alone
+          precompute_cells(bn, ctid - 32 * NWN, (CW - NWN) * 32);
+          if (w == NWN) copy_seed(bn);
+        }
         // full chunks m <= b-1: their records (rows <= 32 b) were final before block b
         bulk_chunks(b, tg, acc);
       }
@@ -1270,33 +1428,35 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
       float rs0[4 * NR];
       if (w == 0 && has_next) load_seed(rs0, ANg + b * DP);
       STX_STAMP(b, 3 + w);
-      named_bar(bar_col, kCW * 32);
-      if (w == 0) STX_STAMP(b, 7);
+      named_bar(bar_col, CW * 32);
+      if (w == 0) STX_STAMP(b, 11);
       if (has_next) {
         // newest chunk (bottoms K0+1 .. K0+32, final after block b's triangle):
-        // warps 0 and 1 take 16 rows each, seeded from W-rows K0 and K0+16, while
-        // warps 2 and 3 precompute block b+1's triangle cells
-        if (w < 2) {
+        // warps 0 .. NWN-1 take 32/NWN rows each, seeded from W-rows K0 (anchor)
+        // and K0 + 32 i / NWN (copied seeds), while the other warps precompute
+        // block b+1's triangle cells
+        if (w < NWN) {
           float rr[4 * NR];
           if (w == 0) {
 #pragma unroll
             for (int i = 0; i < 4 * NR; ++i) rr[i] = rs0[i];
           } else {
-            load_seed(rr, cs.seed + (b & 1) * DP);                           // W-row K0+16
+            load_seed(rr, cs.seed + ((b & 1) * (NWN - 1) + w - 1) * DP);   // W-row K0 + 32 w / NWN
           }
-          rect_run(rr, K0 + 1 + 16 * w, 16, tg, acc);
-        } else {
-          precompute_cells(bn, ctid - 64, 64);
-          if (w == 2) copy_seed(bn);
+          rect_run(rr, K0 + 1 + 32 / NWN * w, 32 / NWN, tg, acc);
+        } else if (CW != 8) {
+          precompute_cells(bn, ctid - 32 * NWN, (CW - NWN) * 32);
+          if (w == NWN) copy_seed(bn);
         }
         cs.part[w * 32 + lane] = merge_part(acc);
         if (ctid == 0) *cs.ctr = 0;
       }
-      STX_STAMP(b, 8 + w);
-      named_bar(bar_col, kCW * 32);
-      if (w == 0) STX_STAMP(b, 12);
+      STX_STAMP(b, 12 + w);
+      named_bar(bar_col, CW * 32);
+      if (w == 0) STX_STAMP(b, 20);
     }
 
+    if (w == 0) STX_STAMP(60, 1);       // blocks done
     // ---------------- backtracking + extraction (a7), warp 0 ------------
     if (w == 0) {
       int c = 0;
@@ -1348,8 +1508,9 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
       }
       __syncwarp();
     }
+    if (w == 0) STX_STAMP(60, 2);       // column written
     first_item = false;
-    named_bar(bar_col, kCW * 32);
+    named_bar(bar_col, CW * 32);
   }
 }
 

@@ -88,6 +88,8 @@ def lib() -> ctypes.CDLL:
         L.stixels_solve.argtypes = [vp, vp, i32, vp, vp, vp]
         L.stixels_sync.argtypes = [vp]
         L.stixels_last_launch_count.argtypes = [vp]
+        L.stixels_query_launch.argtypes = [vp, P(i32), P(i32)]
+        L.stixels_set_launch_plan.argtypes = [vp, i32]
         L.stixels_destroy.argtypes = [vp]
         L.stixels_error_string.argtypes = [i32]
         L.stixels_error_string.restype = ctypes.c_char_p
@@ -104,7 +106,8 @@ DP_DENSE, DP_SPARSE, DP_PAIR2D, DP_INT32, DP_PAIR2D_DENSE = 0, 1, 2, 3, 4
 EXPORTS = ("stixels_default_params", "stixels_create", "stixels_query", "stixels_query_kernel",
            "stixels_compute",
            "stixels_compute_host", "stixels_reduce", "stixels_solve", "stixels_sync",
-           "stixels_last_launch_count", "stixels_destroy", "stixels_error_string",
+           "stixels_last_launch_count", "stixels_query_launch", "stixels_set_launch_plan",
+           "stixels_destroy", "stixels_error_string",
            "stixels_last_error")
 
 
@@ -227,6 +230,16 @@ class Handle:
 
     def last_launch_count(self) -> int:
         return lib().stixels_last_launch_count(self._h)
+
+    def set_launch_plan(self, warps_per_column: int) -> None:
+        """0 = automatic, 4 or 8 warps per column (stixels_set_launch_plan)."""
+        _check(lib().stixels_set_launch_plan(self._h, warps_per_column), self._h)
+
+    def last_launch_shape(self) -> tuple[int, int]:
+        """(warps per column, column groups per CTA) of the last DP launch."""
+        cw, cpc = ctypes.c_int(), ctypes.c_int()
+        _check(lib().stixels_query_launch(self._h, ctypes.byref(cw), ctypes.byref(cpc)), self._h)
+        return cw.value, cpc.value
 
     def destroy(self):
         if getattr(self, "_h", None):

@@ -3,7 +3,7 @@
 build libstixels_trace.so, -DSTX_TRACE).  Prints, per 32-row block b, cycles
 relative to the block start: serial triangle done, build done, each warp's bulk
 end, the bar release, each warp's newest-chunk end, the block end.
-usage (GPU box): python scripts/trace_phases.py [batch]"""
+usage (GPU box): python scripts/trace_phases.py [batch] [warps_per_column]"""
 import ctypes
 import os
 import sys
@@ -29,18 +29,21 @@ disp = torch.from_numpy(pool.view(np.int16)).cuda()[torch.arange(batch) % 16]
 nc = W // 5
 out = torch.empty((batch, nc, H, 12), dtype=torch.uint8, device="cuda")
 cnt = torch.empty((batch, nc), dtype=torch.int32, device="cuda")
-tr = torch.zeros(4 * 64 * 16, dtype=torch.int64, device="cuda")
+tr = torch.zeros(4 * 64 * 32, dtype=torch.int64, device="cuda")
 lib.stixels_trace_buffer(h, ctypes.c_void_p(tr.data_ptr()))
 P = lambda t: ctypes.c_void_p(t.data_ptr())
+cw = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+if cw:
+    assert lib.stixels_set_launch_plan(h, cw) == 0
 for _ in range(2):
     assert lib.stixels_compute(h, P(disp), ctypes.c_int64(W * 2), batch, P(out), P(cnt), None) == 0
 torch.cuda.synchronize()
-t = tr.cpu().numpy().reshape(4, 64, 16).astype(np.int64)
+t = tr.cpu().numpy().reshape(4, 64, 32).astype(np.int64)
 t = t * 1.965          # globaltimer ns -> cycles at 1965 MHz
 nb = (H + 31) // 32
-names = ["setup", "chain", "scans", "tri", "build", "bulk0", "bulk1", "bulk2", "bulk3", "rel1", "new0",
-         "new1", "new2", "new3", "end"]
-slots = [13, 14, 15, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12]
+names = ["setup", "chain", "scans", "tri", "build"] + [f"bulk{i}" for i in range(8)] + ["rel"] + \
+        [f"new{i}" for i in range(8)] + ["end"]
+slots = [21, 22, 23, 1, 2] + list(range(3, 11)) + [11] + list(range(12, 20)) + [20]
 for g in range(4):
     print(f"group {g}: block start-to-start ~cycles (globaltimer ns x 1.965) and phase ends (relative to block start)")
     print("  b  " + " ".join(f"{n:>6s}" for n in names))
@@ -53,3 +56,8 @@ for g in range(4):
         tot += rel[-1]
         print(f" {b:2d}  " + " ".join(f"{x:6d}" for x in rel))
     print(f"  column total {tot} cycles")
+    it = t[g, 60]
+    if it[0]:
+        b0 = t[g, 0, 0]
+        print(f"  item start -> block 0 start {int(b0 - it[0])}, blocks {int(it[1] - b0)}, "
+              f"backtrack+write {int(it[2] - it[1])} cycles")

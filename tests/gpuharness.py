@@ -7,9 +7,11 @@ import numpy as np
 from tests import modelparams as mp
 
 
-def run_gpu(p: dict, frames: np.ndarray, max_batch: int | None = None, host: bool = False):
+def run_gpu(p: dict, frames: np.ndarray, max_batch: int | None = None, host: bool = False,
+            plan: int = 0):
     """frames: [B][H][W] uint16/uint8/float32 -> (lists per frame per column, costs [B][n_cols],
-    counts [B][n_cols], handle)."""
+    counts [B][n_cols], handle).  plan: DP launch plan (0 auto, 4 or 8 warps per column;
+    a forced plan is checked against the launch the library reports)."""
     import torch
     from paper_1610_04124_b200 import stixels as S
     B, H, W = frames.shape
@@ -19,6 +21,8 @@ def run_gpu(p: dict, frames: np.ndarray, max_batch: int | None = None, host: boo
     elif frames.dtype == np.float32:
         params.disp_format = S.F32
     hd = S.Handle(params, W, H, max_batch or B)
+    if plan:
+        hd.set_launch_plan(plan)
     if host:
         out = np.zeros((B, hd.n_cols, hd.cap, 12), np.uint8)
         cnt = np.zeros((B, hd.n_cols), np.int32)
@@ -31,6 +35,8 @@ def run_gpu(p: dict, frames: np.ndarray, max_batch: int | None = None, host: boo
         hd.compute(t, out, cnt, cost)
         hd.sync()
         out, cnt, cost = out.cpu().numpy(), cnt.cpu().numpy(), cost.cpu().numpy()
+    if plan:
+        assert hd.last_launch_shape()[0] == plan, hd.last_launch_shape()
     return S.decode(out, cnt), cost, cnt, hd
 
 

@@ -20,11 +20,27 @@ def _frames_c2(n, seed0=2000, W=1024, H=440, D=128):
 
 
 def _assert_exact(p, frames, **kw):
-    g, gc, cnt, hd = run_gpu(p, frames, **kw)
+    """Both DP launch plans (4 and 8 warps per column) against the oracle."""
+    o, oc = run_oracle(p, frames)
+    for plan in (4, 8):
+        g, gc, cnt, hd = run_gpu(p, frames, plan=plan, **kw)
+        bad = compare_exact(g, gc, o, oc, p["cost_frac_bits"])
+        assert not bad, f"plan {plan}: {len(bad)} mismatching columns, first: {bad[:2]}"
+    return g, gc, cnt, hd
+
+
+def test_single_frame_latency_plan_exact():
+    """One 1024x440 frame (BASELINE configs[1]): the automatic plan gives each
+    column 8 warps (at most 2 columns per SM) and is exact on every column."""
+    frames = _frames_c2(1, seed0=2100)
+    p = mp.make()
+    g, gc, cnt, hd = run_gpu(p, frames)
+    assert hd.last_launch_shape() == (8, 2)
     o, oc = run_oracle(p, frames)
     bad = compare_exact(g, gc, o, oc, p["cost_frac_bits"])
     assert not bad, f"{len(bad)} mismatching columns, first: {bad[:2]}"
-    return g, gc, cnt, hd
+    _, _, _, h4 = run_gpu(p, _frames_c2(4, seed0=2100))
+    assert h4.last_launch_shape() == (4, 4)     # a batch filling the GPU keeps 4 x 4
 
 
 def test_reduce_bit_exact():
@@ -192,7 +208,7 @@ def test_c2_frames_exact():
     frames = _frames_c2(3)
     p = mp.make()
     g, gc, cnt, hd = _assert_exact(p, frames)
-    assert hd.last_launch_count() == 2
+    assert hd.last_launch_count() == 2      # reduce_kernel + dp_kernel
 
 
 def test_dp_variants_exact():
@@ -406,3 +422,93 @@ def test_deterministic_bytes():
     hd.compute(t, o2, c2, k2)
     hd.sync()
     assert torch.equal(o1, o2) and torch.equal(c1, c2) and torch.equal(k1, k2)
+
+
+@pytest.mark.parametrize("fmt,mode,W,s", [("u16", 0, 1027, 5), ("u16", 1, 1024, 5), ("u8", 0, 1040, 3),
+                                          ("f32", 0, 333, 7), ("u16", 1, 128, 13)])
+def test_stage_calls_equal_compute(fmt, mode, W, s):
+    """The stage entry points (stixels_reduce -> stixels_solve) give the same bytes
+    as stixels_compute, and both equal the oracle (exact mode), per input format
+    and reduction."""
+    import torch
+    from paper_1610_04124_b200 import stixels as S
+    H, D = 120, 128
+    rng = np.random.default_rng(77 + s)
+    base = _frames_c2(2, seed0=2300, W=W, H=H)
+    if fmt == "u8":
+        f = (base >> 4).astype(np.uint8)
+        f[base == 0xFFFF] = 255
+        p = mp.make(stixel_width=s, reduce_mode=mode, disp_frac_bits=0, invalid_value=255)
+    elif fmt == "f32":
+        f = np.where(base == 0xFFFF, np.nan, base.astype(np.float32) / 16.0).astype(np.float32)
+        f[rng.random(f.shape) < 0.01] = -1.0
+        p = mp.make(stixel_width=s, reduce_mode=mode, disp_format=S.F32)
+    else:
+        f = base
+        p = mp.make(stixel_width=s, reduce_mode=mode)
+    g, gc, cnt, hd = run_gpu(p, f)
+    assert hd.last_launch_count() == 2
+    # the stage calls on the same handle
+    B = f.shape[0]
+    t = torch.from_numpy(f.view(np.int16) if f.dtype == np.uint16 else f).cuda()
+    cols = torch.empty((B, hd.n_cols, H), dtype=torch.int16, device="cuda")
+    out, cnt2, cost2 = hd.alloc_outputs(B)
+    hd.reduce(t, cols)
+    hd.solve(cols, out, cnt2, cost2)
+    hd.sync()
+    g2 = S.decode(out.cpu().numpy(), cnt2.cpu().numpy())
+    assert g2 == g
+    assert (cost2.cpu().numpy() == gc).all()
+    o, oc = run_oracle(p, f)
+    bad = compare_exact(g, gc, o, oc, p["cost_frac_bits"])
+    assert not bad, f"{len(bad)} mismatching columns, first: {bad[:2]}"
+
+
+@pytest.mark.parametrize("fmt", ["u16", "u8", "f32"])
+@pytest.mark.parametrize("s", [3, 5, 7, 10])
+@pytest.mark.parametrize("pad", [0, 48])
+def test_reduce_rows_kernel_bit_exact(fmt, s, pad):
+    """The row-wise register reduction (reduce_rows_kernel: s in {3, 5, 7, 10}, 16-byte
+    aligned frames), bit-exact against the oracle for mean and median: widths whose
+    last column group overruns a tight row (element loads), padded rows (pitch >
+    W bpp), ragged tails, invalid / out-of-range / negative / NaN pixels."""
+    import torch
+    from oracle import oracle as orc
+    from paper_1610_04124_b200 import stixels as S
+    H, D = 70, 64
+    bpp = {"u16": 2, "u8": 1, "f32": 4}[fmt]
+    W = (16 * 37) // bpp + s - 1                     # a multiple of 16 bytes + a ragged tail
+    W -= ((W * bpp) % 16) // bpp                     # tight rows: W bpp a multiple of 16
+    rng = np.random.default_rng(100 * s + bpp + pad)
+    Wp = W + pad // bpp                              # padded row (pitch)
+    if fmt == "u16":
+        full = rng.integers(0, (D + 2) * 16, size=(2, H, Wp)).astype(np.uint16)
+        full[rng.random(full.shape) < 0.1] = 0xFFFF
+        kw = dict(invalid_value=0xFFFF, disp_frac_bits=4)
+        dev = torch.from_numpy(full.view(np.int16)).cuda()
+    elif fmt == "u8":
+        full = rng.integers(0, 256, size=(2, H, Wp)).astype(np.uint8)
+        kw = dict(invalid_value=255, disp_frac_bits=2, disp_format=S.U8)
+        dev = torch.from_numpy(full).cuda()
+    else:
+        full = (rng.random((2, H, Wp)) * (D + 2) - 1).astype(np.float32)
+        full[rng.random(full.shape) < 0.05] = np.nan
+        kw = dict(disp_format=S.F32)
+        dev = torch.from_numpy(full).cuda()
+    f = np.ascontiguousarray(full[:, :, :W])
+    assert (Wp * bpp) % 16 == 0
+    for mode in (0, 1):
+        p = mp.make(max_disparity=D, stixel_width=s, reduce_mode=mode, **kw)
+        hd = S.Handle(S.params_from_dict(p, H), W, H, 2)
+        cols = torch.empty((2, hd.n_cols, H), dtype=torch.int16, device="cuda")
+        hd.reduce(dev, cols, row_pitch_bytes=Wp * bpp)
+        hd.sync()
+        got = cols.cpu().numpy().view(np.uint16).astype(np.int32)
+        got[got == 0xFFFF] = -1
+        for b in range(2):
+            if fmt == "f32":
+                want = orc.reduce(f[b], s, 0, 0, D, mode=mode)
+            else:
+                want = orc.reduce(f[b], s, kw["disp_frac_bits"], kw["invalid_value"], D, mode=mode)
+            assert (got[b] == want).all(), (mode, b, np.argwhere(got[b] != want)[:3])
+        hd.destroy()
