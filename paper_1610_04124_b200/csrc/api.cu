@@ -589,7 +589,7 @@ static int launch_reduce(stixels_handle* h, const void* d_disp, int64_t pitch, i
   if (r.vec && (r.s == 3 || r.s == 5 || r.s == 7 || r.s == 10)) {
     auto go_rr = [&](auto kern, int G) {
       const int ngroups = (h->n_cols + G - 1) / G;
-      dim3 g((ngroups + kRRWarps - 1) / kRRWarps, (h->H + 31) / 32, batch);
+      dim3 g((ngroups + kRRGroups - 1) / kRRGroups, (h->H + 32 * kRRWarps - 1) / (32 * kRRWarps), batch);
       kern<<<g, 32 * kRRWarps, 0, s>>>(r);
     };
 #define STX_RR(BPPV, SWV)                                                                        \

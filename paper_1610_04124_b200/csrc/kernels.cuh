@@ -189,12 +189,13 @@ __global__ void __launch_bounds__(kRedThreads) reduce_kernel(ReduceArgs a) {
 
 // ---------------------------------------------------------------------------
 // K1 (row-wise variant, the default when its span fits): lanes own consecutive
-// image rows, each thread G = 16 / gcd(16, s bpp) consecutive reduced columns of
-// its row, so its bytes start 16-byte aligned and are NV = G s bpp / 16 vector
+// image rows; a column group is G = 16 / gcd(16, s bpp) consecutive reduced
+// columns, whose bytes start 16-byte aligned and are NV = G s bpp / 16 vector
 // loads straight into registers (no shared-memory tile); the pixels are unpacked
-// at compile-time offsets.  A warp reads 32 rows x NV x 16 bytes (the 32-byte
-// sectors shared by neighbouring spans are L1 hits) and writes, per column, 32
-// consecutive model rows (64 bytes, coalesced).  Same arithmetic as reduce_kernel
+// at compile-time offsets.  Each warp walks kRRGroups groups of its 32 rows with
+// the next group's loads in flight while it reduces the current one (a sector
+// shared by two consecutive spans is an L1 hit of the same lane), and writes, per
+// column, 32 consecutive model rows (64 bytes, coalesced).  Same arithmetic as reduce_kernel
 // (decode and validity L#23/L#28, mean P:195 or median L#24, half-up rounding to
 // 1/256, the L#27 clamp); the rounding division is a multiply-high by a per-CTA
 // table floor(2^32 / d) and one correction step.
@@ -207,8 +208,10 @@ struct RowRed {
 };
 constexpr int kRRWarps = 8;                              // warps (column groups) per CTA
 
+constexpr int kRRGroups = 8;                             // column groups per warp (loop)
+
 template <bool MEDIAN, int BPP, int SW>
-__global__ void __launch_bounds__(32 * kRRWarps) reduce_rows_kernel(ReduceArgs a) {
+__global__ void __launch_bounds__(32 * kRRWarps, 4) reduce_rows_kernel(ReduceArgs a) {
   using RR = RowRed<BPP, SW>;
   constexpr int G = RR::G, NV = RR::NV;
   __shared__ uint32_t rcp[2 * SW + 2];
@@ -216,87 +219,101 @@ __global__ void __launch_bounds__(32 * kRRWarps) reduce_rows_kernel(ReduceArgs a
     rcp[i] = i < 2 ? 0u : (uint32_t)((1ull << 32) / (unsigned)i);
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  const int cg = blockIdx.x * kRRWarps + (threadIdx.x >> 5);      // column group
-  const int r = blockIdx.y * 32 + lane;                           // image row
+  const int r = (blockIdx.y * kRRWarps + (threadIdx.x >> 5)) * 32 + lane;   // image row
   const int frame = blockIdx.z;
-  const int c0 = cg * G;
-  if (c0 >= a.n_cols || r >= a.H) return;
-  const int64_t sb = (int64_t)c0 * SW * BPP;                      // span start (16-byte aligned)
+  if (r >= a.H) return;
+  const int cg0 = blockIdx.x * kRRGroups;
+  const int cg1 = min(cg0 + kRRGroups, (a.n_cols + G - 1) / G);
   const uint8_t* row = a.disp + ((int64_t)frame * a.H + r) * a.pitch;
-  uint32_t wv[NV * 4];
-  if (sb + NV * 16 <= a.pitch) {
-#pragma unroll
-    for (int i = 0; i < NV; ++i) {
-      const uint4 x = __ldg(reinterpret_cast<const uint4*>(row + sb) + i);
-      wv[4 * i] = x.x; wv[4 * i + 1] = x.y; wv[4 * i + 2] = x.z; wv[4 * i + 3] = x.w;
-    }
-  } else {
-    // the last group of a tight row: element loads within [0, W bpp)
-#pragma unroll
-    for (int i = 0; i < NV * 4; ++i) wv[i] = 0u;
-    const int lim_b = a.W * BPP - (int)sb;
-#pragma unroll
-    for (int e = 0; e < NV * 16 / BPP; ++e) {
-      if (e * BPP < lim_b) {
-        uint32_t x;
-        if constexpr (BPP == 4) x = __ldg(reinterpret_cast<const uint32_t*>(row + sb) + e);
-        else if constexpr (BPP == 2) x = __ldg(reinterpret_cast<const uint16_t*>(row + sb) + e);
-        else x = __ldg(row + sb + e);
-        wv[(e * BPP) >> 2] |= x << (8 * ((e * BPP) & 3));
-      }
-    }
-  }
   const uint32_t lim = (uint32_t)a.D << a.q_bits;
   const int shift = kRBits + 1 - a.q_bits;
   const float Df = (float)a.D;
   const int v = a.H - 1 - r;
-  uint16_t* out = a.out + ((int64_t)frame * a.n_cols + c0) * a.H + v;
+  const bool inv_hi = a.invalid >= lim;
+  // the span of column group cg into registers: NV vector loads, or element loads
+  // within [0, W bpp) when it would overrun the row's pitch
+  auto load_span = [&](int cg, uint32_t (&wv)[NV * 4]) {
+    const int64_t sb = (int64_t)cg * G * SW * BPP;
+    if (sb + NV * 16 <= a.pitch) {
 #pragma unroll
-  for (int g = 0; g < G; ++g) {
-    if (c0 + g >= a.n_cols) break;
-    uint32_t u[SW];
-    bool ok[SW];
-    uint32_t sum = 0, n = 0;
-#pragma unroll
-    for (int x = 0; x < SW; ++x) {
-      const int e = g * SW + x;                          // pixel index in the span
-      const uint32_t w = wv[(e * BPP) >> 2];
-      if constexpr (BPP == 4) {
-        const float d = __uint_as_float(w);
-        ok[x] = d >= 0.f && d < Df;                      // false for NaN and +-inf too
-        u[x] = ok[x] ? (uint32_t)__float2int_rd(d * 256.f + 0.5f) : 0u;   // L#28
-      } else {
-        u[x] = BPP == 2 ? ((w >> (8 * ((e * 2) & 3))) & 0xffffu) : ((w >> (8 * (e & 3))) & 0xffu);
-        ok[x] = (u[x] != a.invalid) && (u[x] < lim);
+      for (int i = 0; i < NV; ++i) {
+        const uint4 x = __ldg(reinterpret_cast<const uint4*>(row + sb) + i);
+        wv[4 * i] = x.x; wv[4 * i + 1] = x.y; wv[4 * i + 2] = x.z; wv[4 * i + 3] = x.w;
       }
-      sum += ok[x] ? u[x] : 0u;
-      n += ok[x] ? 1u : 0u;
+    } else {
+#pragma unroll
+      for (int i = 0; i < NV * 4; ++i) wv[i] = 0u;
+      const int lim_b = a.W * BPP - (int)sb;
+#pragma unroll
+      for (int e = 0; e < NV * 16 / BPP; ++e) {
+        if (e * BPP < lim_b) {
+          uint32_t x;
+          if constexpr (BPP == 4) x = __ldg(reinterpret_cast<const uint32_t*>(row + sb) + e);
+          else if constexpr (BPP == 2) x = __ldg(reinterpret_cast<const uint16_t*>(row + sb) + e);
+          else x = __ldg(row + sb + e);
+          wv[(e * BPP) >> 2] |= x << (8 * ((e * BPP) & 3));
+        }
+      }
     }
-    if (MEDIAN && n) {
-      const uint32_t k1 = (n - 1) >> 1, k2 = n >> 1;
-      uint32_t va = 0, vb = 0;
+  };
+  uint32_t cur[NV * 4], nxt[NV * 4];
+  if (cg0 < cg1) load_span(cg0, cur);
+  for (int cg = cg0; cg < cg1; ++cg) {
+    if (cg + 1 < cg1) load_span(cg + 1, nxt);         // prefetch: loads stay in flight
+    const int c0 = cg * G;
+    uint16_t* out = a.out + ((int64_t)frame * a.n_cols + c0) * a.H + v;
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      if (c0 + g >= a.n_cols) break;
+      uint32_t u[SW];
+      bool ok[SW];
+      // sum and count of the valid pixels packed in one word: count in bits 24..,
+      // sum (< SW 2^17 <= 2^21 for SW <= 16) below
+      uint32_t sn = 0;
 #pragma unroll
       for (int x = 0; x < SW; ++x) {
-        uint32_t less = 0, leq = 0;
-#pragma unroll
-        for (int y = 0; y < SW; ++y) {
-          less += (ok[y] && u[y] < u[x]) ? 1u : 0u;
-          leq += (ok[y] && u[y] <= u[x]) ? 1u : 0u;
+        const int e = g * SW + x;                        // pixel index in the span
+        const uint32_t w = cur[(e * BPP) >> 2];
+        if constexpr (BPP == 4) {
+          const float d = __uint_as_float(w);
+          ok[x] = d >= 0.f && d < Df;                    // false for NaN and +-inf too
+          u[x] = ok[x] ? (uint32_t)__float2int_rd(d * 256.f + 0.5f) : 0u;   // L#28
+        } else {
+          u[x] = BPP == 2 ? ((w >> (8 * ((e * 2) & 3))) & 0xffffu) : ((w >> (8 * (e & 3))) & 0xffu);
+          // (the sentinel test is redundant when it is >= the range limit)
+          ok[x] = (inv_hi || u[x] != a.invalid) && (u[x] < lim);
         }
-        if (ok[x] && less <= k1 && k1 < leq) va = u[x];
-        if (ok[x] && less <= k2 && k2 < leq) vb = u[x];
+        sn += ok[x] ? u[x] + (1u << 24) : 0u;
       }
-      sum = va + vb;
-      n = 2;
+      uint32_t sum = sn & 0xffffffu, n = sn >> 24;
+      if (MEDIAN && n) {
+        const uint32_t k1 = (n - 1) >> 1, k2 = n >> 1;
+        uint32_t va = 0, vb = 0;
+#pragma unroll
+        for (int x = 0; x < SW; ++x) {
+          uint32_t less = 0, leq = 0;
+#pragma unroll
+          for (int y = 0; y < SW; ++y) {
+            less += (ok[y] && u[y] < u[x]) ? 1u : 0u;
+            leq += (ok[y] && u[y] <= u[x]) ? 1u : 0u;
+          }
+          if (ok[x] && less <= k1 && k1 < leq) va = u[x];
+          if (ok[x] && less <= k2 && k2 < leq) vb = u[x];
+        }
+        sum = va + vb;
+        n = 2;
+      }
+      uint16_t val = 0xFFFF;
+      if (n) {
+        const uint32_t num = (sum << shift) + n, d = 2u * n;   // num < 2^32: sum < SW 2^16
+        uint32_t q = __umulhi(num, rcp[d]);
+        if (num - q * d >= d) ++q;                        // floor(2^32/d) under-estimates by <= 1
+        val = (uint16_t)min(q, ((uint32_t)(a.D - 1) << kRBits) + (1u << (kRBits - 1)) - 1u);
+      }
+      out[(int64_t)g * a.H] = val;
     }
-    uint16_t val = 0xFFFF;
-    if (n) {
-      const uint32_t num = (sum << shift) + n, d = 2u * n;   // num < 2^32: sum < SW 2^16
-      uint32_t q = __umulhi(num, rcp[d]);
-      if (num - q * d >= d) ++q;                          // floor(2^32/d) under-estimates by <= 1
-      val = (uint16_t)min(q, ((uint32_t)(a.D - 1) << kRBits) + (1u << (kRBits - 1)) - 1u);
-    }
-    out[(int64_t)g * a.H] = val;
+#pragma unroll
+    for (int i = 0; i < NV * 4; ++i) cur[i] = nxt[i];
   }
 }
 
