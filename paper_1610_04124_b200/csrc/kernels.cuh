@@ -421,7 +421,9 @@ struct ColSmem {
                     //                16-byte record each (one LDS.128 in the serial chain):
                     //                {object data term, the same plus its O-above-G prior
                     //                (gravity level), object mean f (int bits), unused}
-  uint4* rec;       // [h+3][2]       row j: {AO0,AO1,AGm,AGh} {T[j], N4[j], AGl, ordthr | drp<<16}
+  uint4* rec;       // [h+3][2]       row j: {V0,V1,V2,V3} {T[j], N4[j], b1 | b2<<16, b3 | cb<<10 | drp<<16}
+                    //                (the prior of a bottom-j candidate as a step function of
+                    //                the object mean f: V_i on [b_i, b_i+1), see write_record)
                     //                ({T, N4} also read per lane as a uint2: tn_at)
   uint32_t* eo;     // [h+2]          lo16: ring window byte offset; hi16: E0 byte offset
   uint16_t* argO;   // [h]            j | c'<<12
@@ -562,17 +564,19 @@ __device__ __forceinline__ float ldsf(uint32_t addr) {
 
 // Per-row uniform values of record j for the cell evaluation.
 struct RowU {
-  float AO0, AO1, AGm, AGh, AGl;   // predecessor terms of row j, shifted by -cap*j
+  float V0, V1, V2, V3;            // min over predecessor classes of (C[j-1] + prior), shifted
+                                   // by -cap*j, for f < b1, [b1, b2), [b2, b3), >= b3
   uint32_t T, N4;
-  int ordthr, drp;                 // drp = round(d_j) + 1, no_band<DP>() if pixel j is invalid
+  int b1, b2, b3, cb;              // breakpoints; cb bit i: the winner of interval i is O (else G)
+  int drp;                         // drp = round(d_j) + 1, no_band<DP>() if pixel j is invalid
 };
 __device__ __forceinline__ RowU unpack_row(uint4 x, uint4 y) {
   RowU u;
-  u.AO0 = __uint_as_float(x.x); u.AO1 = __uint_as_float(x.y);
-  u.AGm = __uint_as_float(x.z); u.AGh = __uint_as_float(x.w);
+  u.V0 = __uint_as_float(x.x); u.V1 = __uint_as_float(x.y);
+  u.V2 = __uint_as_float(x.z); u.V3 = __uint_as_float(x.w);
   u.T = y.x; u.N4 = y.y;
-  u.AGl = __uint_as_float(y.z);
-  u.ordthr = (int)(y.w & 0xffffu); u.drp = (int)(y.w >> 16);
+  u.b1 = (int)(y.z & 0xffffu); u.b2 = (int)(y.z >> 16);
+  u.b3 = (int)(y.w & 0x3ffu); u.cb = (int)((y.w >> 10) & 0xfu); u.drp = (int)(y.w >> 16);
   return u;
 }
 __device__ __forceinline__ RowU load_row(const uint4* rec, int j) {
@@ -783,17 +787,14 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
       const uint4* q = shp<const uint4>(rec_s + 32u * (uint32_t)j);
       return unpack_row(q[0], q[1]);
     };
-    auto cell = [&](const RowU& r, int j, int thA, int thB, int f, CT p, CT w, CT& best, int& argj) {
+    // the candidate's prior: the row's step function of f (3 compares, 3 selects)
+    auto cell = [&](const RowU& r, int j, int f, CT p, CT w, CT& best, int& argj) {
+      const float pr = (f >= r.b2) ? ((f >= r.b3) ? r.V3 : r.V2) : ((f >= r.b1) ? r.V1 : r.V0);
       if constexpr (IW) {              // records hold scaled int32 quanta (bits in the float fields)
-        const int aO = (f > r.ordthr) ? __float_as_int(r.AO1) : __float_as_int(r.AO0);
-        const int aG = (f >= thA) ? __float_as_int(r.AGh)
-                                  : ((f < thB) ? __float_as_int(r.AGl) : __float_as_int(r.AGm));
-        best = min(best, p - w + min(aO, aG));   // (cost x 32) | bottom offset: run minimum
+        best = min(best, p - w + __float_as_int(pr));   // (cost x 32) | bottom offset: run minimum
         (void)argj; (void)j;
       } else {
-        float aO = (f > r.ordthr) ? r.AO1 : r.AO0;
-        float aG = (f >= thA) ? r.AGh : ((f < thB) ? r.AGl : r.AGm);
-        float cand = (p - w) + fminf(aO, aG);
+        float cand = (p - w) + pr;
         if (cand < best) { best = cand; argj = j; }
       }
     };
@@ -853,17 +854,15 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
         // pad before M2) and is never used.
         const RowU n = rowj(jm + 2);
         const int g0 = fmean(n, tg.T0, tg.N0), g1 = fmean(n, tg.T1, tg.N1);
-        const int2 th = *shp<const int2>(thr_s + 8u * (uint32_t)jm);
-        const int thA = th.x, thB = th.y;
         const uint32_t wb = SPARSE ? wbuf_s : ring_s + (hw ? ((2 + 2 * half) & 3) : ((1 + 2 * half) & 3)) * DP * 4u;
         const CT p0 = *shp<const CT>(tg.pp0 + 4u * f0), p1 = *shp<const CT>(tg.pp1 + 4u * f1);
         const CT w0 = *shp<const CT>(wb + 4u * f0), w1 = *shp<const CT>(wb + 4u * f1);
         if constexpr (IW) {
-          cell(r, jm, thA, thB, f0, p0, w0, m0, acc.a0);
-          cell(r, jm, thA, thB, f1, p1, w1, m1, acc.a1);
+          cell(r, jm, f0, p0, w0, m0, acc.a0);
+          cell(r, jm, f1, p1, w1, m1, acc.a1);
         } else {
-          cell(r, jm, thA, thB, f0, p0, w0, acc.b0, acc.a0);
-          cell(r, jm, thA, thB, f1, p1, w1, acc.b1, acc.a1);
+          cell(r, jm, f0, p0, w0, acc.b0, acc.a0);
+          cell(r, jm, f1, p1, w1, acc.b1, acc.a1);
         }
         if constexpr (SPARSE && IW) {
           __syncwarp();
@@ -1197,11 +1196,8 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
         } else {
           const RowU r = load_row(cs.rec, argj);
           argf = span_f(Tk - r.T, N4k - r.N4, smem, Dm1);
-          const uint32_t th = __ldg(a.thrg + argj);
-          float aO = (argf > r.ordthr) ? r.AO1 : r.AO0;
-          float aG = (argf >= (int)(th & 0xffffu)) ? r.AGh : ((argf < (int)(th >> 16)) ? r.AGl : r.AGm);
-          if constexpr (IW) argc = (__float_as_int(aG) <= __float_as_int(aO)) ? 0 : 1;   // int32 records
-          else argc = (aG <= aO) ? 0 : 1;
+          const int iv = (argf >= r.b1) + (argf >= r.b2) + (argf >= r.b3);   // the step's interval
+          argc = (r.cb >> iv) & 1;
         }
         const float kOG = a.kOG;
         const int om = a.ord_margin;
@@ -1393,11 +1389,31 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
             if constexpr (IW) return (uint32_t)((x >= 16777216.f ? kIWBig : __float2int_rn(x) * kIWS) + (k & 31));
             else return __float_as_uint(x);
           };
-          cs.rec[2 * (k + 1)] = make_uint4(rb((best + a.kOO_lo) - sh), rb((best + a.kOO_hi) - sh),
-                                           rb((CGk + a.kGO_mid) - sh), rb((CGk + a.kGO_hi) - sh));
+          // prior of a candidate with bottom j = k + 1 as a function of its object
+          // mean f: O below (ordering: f > argf + om), G below (gravity: f >= thA,
+          // diving: f < thB, L#1, L#15), the cheaper of the two (L#17: G on ties)
+          const uint32_t AO0 = rb((best + a.kOO_lo) - sh), AO1 = rb((best + a.kOO_hi) - sh);
+          const uint32_t AGm = rb((CGk + a.kGO_mid) - sh), AGh = rb((CGk + a.kGO_hi) - sh);
+          const uint32_t AGl = rb((CGk + a.kGO_lo) - sh);
+          const int2 th = thrS[k + 1];
+          const int bO = min(argf + a.ord_margin + 1, 1023);          // f > argf + om
+          const int b1 = min(bO, min(th.x, th.y)), b3 = max(bO, max(th.x, th.y));
+          const int b2 = max(min(bO, th.x), min(max(bO, th.x), th.y));
+          int cb = 0;
+          auto step = [&](int f, int i) {
+            const uint32_t aO = (f >= bO) ? AO1 : AO0;
+            const uint32_t aG = (f >= th.x) ? AGh : ((f >= th.y) ? AGm : AGl);
+            bool g;
+            if constexpr (IW) g = (int)aG <= (int)aO;
+            else g = __uint_as_float(aG) <= __uint_as_float(aO);
+            cb |= (g ? 0 : 1) << i;
+            return g ? aG : aO;
+          };
+          const uint32_t V0 = step(b1 - 1, 0), V1 = step(b1, 1), V2 = step(b2, 2), V3 = step(b3, 3);
+          cs.rec[2 * (k + 1)] = make_uint4(V0, V1, V2, V3);
           uint32_t* ry = reinterpret_cast<uint32_t*>(cs.rec + 2 * (k + 1) + 1);
-          ry[2] = rb((CGk + a.kGO_lo) - sh);
-          reinterpret_cast<uint16_t*>(ry + 3)[0] = (uint16_t)(argf + a.ord_margin);   // ordthr (drp kept)
+          ry[2] = (uint32_t)b1 | ((uint32_t)b2 << 16);
+          reinterpret_cast<uint16_t*>(ry + 3)[0] = (uint16_t)(b3 | (cb << 10));   // (drp kept)
           cs.argO[k] = (uint16_t)(argj | (argc << 12));
           cs.argG[k] = (uint16_t)aG;
           cs.argS[k] = (uint16_t)aS;
