@@ -206,10 +206,12 @@ int stixels_compute_host(stixels_handle* h, const void* h_disp, int64_t row_pitc
  *           0xFFFF = invalid (a1-a2). */
 int stixels_reduce(stixels_handle* h, const void* d_disp, int64_t row_pitch_bytes, int batch,
                    uint16_t* d_cols);
-/*  reduce clamps every value below D - 1/2 (to at most (D-1)*256 + 127) so
- *  that its integer rounding indexes the D x D pair LUT (L#27).
- *  solve  : d_cols (as produced by stixels_reduce) -> stixels (a3-a7); larger
- *           values are clamped the same way on load. */
+/*  Values are not clamped (L#27: only the object model clamps a
+ *  pixel below D - 1/2, so that its rounding indexes the D x D pair LUT of
+ *  P:175); the one limit is 0xFFFE (reachable only at D = 256 with 8
+ *  fractional input bits), since 0xFFFF marks an invalid value.
+ *  solve  : d_cols (as produced by stixels_reduce) -> stixels (a3-a7); a value
+ *           >= D * 256 is invalid (L#23). */
 int stixels_solve(stixels_handle* h, const uint16_t* d_cols, int batch, stixel_t* d_out,
                   int32_t* d_count, float* d_col_cost);
 

@@ -124,9 +124,10 @@ long long orc_ground_R(const orc_model* m, int v) {
  * Input: raw fixed-point disparities with Q_bits fractional bits (a1); a pixel
  * is invalid if it equals `invalid` or decodes to >= D (L#23).
  * Output: out[c*H + v] = round_half_up(2^R_bits * sum / (2^Q_bits * n)) in
- * units of 1/2^R_bits, v = H-1-r (model row from the bottom), or -1 = invalid,
- * clamped to below D - 1/2 (L#27): the pair LUT of P:175 is D x D, so a
- * pixel's integer disparity round_half_up(d') must lie in [0, D).
+ * units of 1/2^R_bits, v = H-1-r (model row from the bottom), or -1 = invalid.
+ * Not clamped (L#27: only the object model clamps, see object_disp); the one
+ * representational limit is 0xFFFE (reduced columns are 16-bit with 0xFFFF =
+ * invalid in the C ABI; reachable only at D = 256 with 8 fractional input bits).
  * ------------------------------------------------------------------------ */
 /* One input pixel (a1).  u8/u16: the raw fixed-point value (Q_bits fractional
  * bits), invalid if it equals `invalid` or decodes to >= D.  f32 (bytes_per_px 4,
@@ -149,8 +150,8 @@ static int pixel_value(const void* img, int bytes_per_px, long long idx, unsigne
 }
 
 static int clamp_reduced(long long x, int D, int R_bits) {
-  long long mx = ((long long)(D - 1) << R_bits) + (1LL << (R_bits - 1)) - 1;
-  return (int)(x < mx ? x : mx);
+  (void)D; (void)R_bits;
+  return (int)(x < 0xFFFE ? x : 0xFFFE);
 }
 void orc_reduce(const void* img, int bytes_per_px, int W, int H, long long pitch_px, int s,
                 int Q_bits, unsigned int invalid, int D, int R_bits, int* out) {
@@ -185,8 +186,8 @@ void orc_reduce(const void* img, int bytes_per_px, int W, int H, long long pitch
  * of the VALID pixels among the s of a row segment -- the middle value of the
  * sorted valid values, the mean of the two middle values when their count is
  * even -- in units of 1/2^R_bits, rounded half up exactly like the mean
- * (orc_reduce with the middle value(s) as the summands) and clamped the same
- * way (L#27).  All invalid -> -1.
+ * (orc_reduce with the middle value(s) as the summands), with the same
+ * 0xFFFE limit.  All invalid -> -1.
  * Written the plain way: collect, sort (qsort), pick.
  * ------------------------------------------------------------------------ */
 static int cmp_uint(const void* a, const void* b) {
@@ -250,16 +251,26 @@ double orc_cost_sky(const orc_model* m, int dR) {
 int orc_round_disp(const orc_model* m, int dR) {
   return (dR + (1 << (m->R_bits - 1))) >> m->R_bits;
 }
+/* The pixel disparity as the object model sees it (L#27): the pair LUT of P:175
+ * is D x D ("all possible pairs of pixel disparity and mean disparity"), so the
+ * object model takes d' clamped below D - 1/2, where its half-up rounding is
+ * D - 1; its LUT index and its span mean use this value.  Ground and
+ * sky (Eq. 4) use d' itself. */
+static int object_disp(const orc_model* m, int dR) {
+  int mx = ((m->D - 1) << m->R_bits) + (1 << (m->R_bits - 1)) - 1;
+  return dR < mx ? dR : mx;
+}
 double orc_cost_object(const orc_model* m, int dR, int f) {
   if (dR < 0) return qz(m, cap_cost(m));
-  double delta = (double)(orc_round_disp(m, dR) - f);
+  double delta = (double)(orc_round_disp(m, object_disp(m, dR)) - f);
   return qz(m, orc_eq4(m, delta, m->sigma_o_f ? m->sigma_o_f[f] : m->sigma[ORC_O]));
 }
 
 /* --------------------------------------------------------------------------
  * Object model value f_n ("the mean of the measured disparities of the
  * considered stixel"), rounded to an integer, half up (L#10), in exact
- * integer arithmetic, clamped to [0, D-1]; 0 if the span has no valid pixel
+ * integer arithmetic, of the object disparities object_disp (L#27; hence in
+ * [0, D-1], the clamp below is a guard); 0 if the span has no valid pixel
  * (L#11).  From the span's disparity sum S (units 1/2^R) and valid count n.
  * ------------------------------------------------------------------------ */
 static int mean_from_sums(const orc_model* m, long long S, long long n) {
@@ -274,7 +285,7 @@ int orc_span_mean(const orc_model* m, const int* col, int vb, int vt) {
   long long S = 0, n = 0;
   for (int v = vb; v <= vt; ++v) {
     if (col[v] < 0) continue;
-    S += col[v];
+    S += object_disp(m, col[v]);
     n += 1;
   }
   return mean_from_sums(m, S, n);
@@ -397,7 +408,7 @@ int orc_solve_column(const orc_model* m, const int* col, int mode, orc_stixel* o
       PS[v + 1] = PS[v] + orc_cost_sky(m, col[v]);
       for (int f = 0; f < m->D; ++f)
         PO[(size_t)f * (h + 1) + v + 1] = PO[(size_t)f * (h + 1) + v] + orc_cost_object(m, col[v], f);
-      PD[v + 1] = PD[v] + (col[v] >= 0 ? col[v] : 0);
+      PD[v + 1] = PD[v] + (col[v] >= 0 ? object_disp(m, col[v]) : 0);
       PN[v + 1] = PN[v] + (col[v] >= 0 ? 1 : 0);
       gR[v] = orc_ground_R(m, v);
     }

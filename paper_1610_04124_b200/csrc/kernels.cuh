@@ -178,8 +178,9 @@ __global__ void __launch_bounds__(kRedThreads) reduce_kernel(ReduceArgs a) {
       } else {
         q = (uint32_t)((((uint64_t)sum << shift) + n) / (2ull * n));
       }
-      // below D - 1/2 (L#27): the pixel's integer disparity indexes the D x D LUT
-      val = (uint16_t)min(q, ((uint32_t)(a.D - 1) << kRBits) + (1u << (kRBits - 1)) - 1u);
+      // 16-bit columns, 0xFFFF = invalid: the top value 65535 (D = 256 with 8
+      // fractional input bits only) is stored as 0xFFFE (L#27)
+      val = (uint16_t)min(q, 0xFFFEu);
     }
     const int r = r0 + rr;
     const int v = a.H - 1 - r;
@@ -197,7 +198,7 @@ __global__ void __launch_bounds__(kRedThreads) reduce_kernel(ReduceArgs a) {
 // shared by two consecutive spans is an L1 hit of the same lane), and writes, per
 // column, 32 consecutive model rows (64 bytes, coalesced).  Same arithmetic as reduce_kernel
 // (decode and validity L#23/L#28, mean P:195 or median L#24, half-up rounding to
-// 1/256, the L#27 clamp); the rounding division is a multiply-high by a per-CTA
+// 1/256, the 0xFFFE limit of L#27); the rounding division is a multiply-high by a per-CTA
 // table floor(2^32 / d) and one correction step.
 // ---------------------------------------------------------------------------
 __host__ __device__ constexpr int rr_gcd(int x, int y) { return y == 0 ? x : rr_gcd(y, x % y); }
@@ -308,7 +309,7 @@ __global__ void __launch_bounds__(32 * kRRWarps, 4) reduce_rows_kernel(ReduceArg
         const uint32_t num = (sum << shift) + n, d = 2u * n;   // num < 2^32: sum < SW 2^16
         uint32_t q = __umulhi(num, rcp[d]);
         if (num - q * d >= d) ++q;                        // floor(2^32/d) under-estimates by <= 1
-        val = (uint16_t)min(q, ((uint32_t)(a.D - 1) << kRBits) + (1u << (kRBits - 1)) - 1u);
+        val = (uint16_t)min(q, 0xFFFEu);                   // (0xFFFF = invalid, L#27)
       }
       out[(int64_t)g * a.H] = val;
     }
@@ -541,7 +542,7 @@ constexpr int kM2Pad = 16;          // bytes of shared memory before the M2 tabl
 // Object model value f of span [j, k] from prefix differences:
 // f = floor(t / (256 n)), t = sum(d + 128) over valid pixels: the exact half-up
 // rounded mean (L#10), via a multiply-high by ceil(2^31/n) (exact for t < 2^28).
-// No clamp is needed: every reduced value is below D - 1/2 (L#27), so is their
+// No clamp is needed: every object disparity is below D - 1/2 (L#27), so is their
 // rounded mean.  n4 = 4n is the byte offset into M2 (kM2Pad bytes into dynamic smem).
 __device__ __forceinline__ int span_f(uint32_t t, uint32_t n4, const uint8_t* smem0, int Dm1) {
   uint32_t y = t >> (kRBits - 1);
@@ -801,7 +802,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
     auto fmean = [&](const RowU& r, uint32_t Tk, uint32_t N4k) {
       const uint32_t n4 = N4k - r.N4;
       const uint32_t M = *shp<const uint32_t>(m2_s + n4);
-      return (int)__umulhi((Tk - r.T) >> (kRBits - 1), M);   // < D: inputs below D - 1/2 (L#27)
+      return (int)__umulhi((Tk - r.T) >> (kRBits - 1), M);   // < D: object disparities below D - 1/2 (L#27)
     };
     auto band_i = [&](int drp) {
       atomicAdd(shp<int>(ibase_s + 4u * (uint32_t)drp), -iwt);
@@ -946,7 +947,11 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
     // one row v of prologue A from its reduced value dR (-1 invalid)
     auto prologue_row = [&](int v, int dR) {
       const bool valid = dR >= 0;
-      const int dr = valid ? (dR + (1 << (kRBits - 1))) >> kRBits : -1;   // round half up (L#9)
+      // the object model's view of the pixel (L#27): clamped below D - 1/2, so its
+      // rounding (the pair-LUT index, L#9) and every span mean lie in [0, D);
+      // ground and sky use dR itself (Eq. 4)
+      const int dO = min(dR, ((a.D - 1) << kRBits) + (1 << (kRBits - 1)) - 1);
+      const int dr = valid ? (dO + (1 << (kRBits - 1))) >> kRBits : -1;   // round half up (L#9)
       if (v < h) {
         float xg = capQ, xs = capQ;
         if (valid) {
@@ -955,7 +960,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
           xs = __ldg(a.gS + min(dR, a.LS - 1));
         }
         tG[v] = xg; tS[v] = xs;
-        tD[v] = valid ? (uint32_t)dR + (1u << (kRBits - 1)) : 0u;
+        tD[v] = valid ? (uint32_t)dO + (1u << (kRBits - 1)) : 0u;
       }
       if (v <= h)                        // static record word of row v: pixel code (ordthr later)
         cs.rec[2 * v + 1].w = (uint32_t)(valid ? dr + 1 : kNoBand) << 16;
@@ -975,10 +980,9 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
     for (int v = ctid; v < h + 2; v += CW * 32) {
       int dR = -1;
       if (v < h) {
-        uint32_t u = col[v];
-        // (clamped below D - 1/2 as stixels_reduce does, L#27, so caller-made
-        // columns cannot push an object mean past the table)
-        dR = (u == 0xffffu) ? -1 : min((int)u, ((a.D - 1) << kRBits) + (1 << (kRBits - 1)) - 1);
+        const uint32_t u = col[v];
+        // valid below D (L#23: a caller-made column value >= D * 256 is invalid)
+        dR = (u == 0xffffu || u >= ((uint32_t)a.D << kRBits)) ? -1 : (int)u;
       }
       prologue_row(v, dR);
     }

@@ -47,9 +47,11 @@ def solve(m, col):
         return 0 if x <= 0 else math.floor(x * 256 + 0.5)
 
     val = [None if d < 0 else d for d in col]
+    # the object model sees pixels clamped below D - 1/2 (L#27)
+    obj = [None if d is None else min(d, (D - 1) * 256 + 127) for d in val]
 
     def mean(j, k):
-        vs = [d for d in val[j:k + 1] if d is not None]
+        vs = [d for d in obj[j:k + 1] if d is not None]
         if not vs:
             return 0
         return min(D - 1, math.floor(Fraction(sum(vs), 256 * len(vs)) + Fraction(1, 2)))
@@ -63,7 +65,7 @@ def solve(m, col):
             elif c == S:
                 tot += pixel(None if d is None else Fraction(d, 256), 0, m.sigma[S])
             else:
-                tot += pixel(None if d is None else (d + 128) // 256, f, m.sigma[O])
+                tot += pixel(None if d is None else (obj[v] + 128) // 256, f, m.sigma[O])
         return tot
 
     bic = nlp(m.p_exist)

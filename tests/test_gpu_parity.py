@@ -512,3 +512,21 @@ def test_reduce_rows_kernel_bit_exact(fmt, s, pad):
                 want = orc.reduce(f[b], s, kw["disp_frac_bits"], kw["invalid_value"], D, mode=mode)
             assert (got[b] == want).all(), (mode, b, np.argwhere(got[b] != want)[:3])
         hd.destroy()
+
+
+@pytest.mark.parametrize("D,q", [(64, 4), (256, 8)])
+def test_top_of_range_pixels_exact(D, q):
+    """L#27: pixels in [D - 1/2, D) keep their value for the ground and sky terms
+    and are clamped below D - 1/2 only by the object model (its LUT index and span
+    mean); at D = 256 with 8 fractional bits the 16-bit top value is 0xFFFE.
+    Exact against the oracle on frames whose objects sit at the top of the range."""
+    H, W = 96, 160
+    rng = np.random.default_rng(31 + D)
+    top = (D << q) - 1
+    f = rng.integers((D - 2) << q, top + 1, size=(2, H, W)).astype(np.uint16)   # in [D-2, D)
+    f[:, : H // 3] = rng.integers(0, 4 << q, size=(2, H // 3, W))               # a low band
+    f[rng.random(f.shape) < 0.05] = 0xFFFF if q < 8 else 0                       # invalid
+    f[:, :, :20] = top                                                           # d' = D - 2^-q
+    p = mp.make(max_disparity=D, disp_frac_bits=q, invalid_value=0xFFFF if q < 8 else 0,
+                ground_slope=D / (2.0 * H), cost_frac_bits=10 if D > 128 else 11)
+    _assert_exact(p, f)

@@ -102,17 +102,28 @@ def test_reduce_spec_examples():
             assert out.shape == (case["n_cols"], case["h"])
 
 
-def test_reduce_clamps_below_d_minus_half():
-    """L#27: the reduced disparity stays below D - 1/2, so its integer rounding
-    (the pair-LUT index, L#9) lies in [0, D) -- the D x D LUT of P:175."""
+def test_l27_only_the_object_model_clamps():
+    """L#27: the reduction does not clamp (the pixel keeps d' in [D - 1/2, D) for
+    the ground and sky terms of Eq. 4); the object model sees the pixel
+    clamped below D - 1/2, so its pair-LUT index (L#9) is D - 1, the top of the
+    D x D table of, and its span mean is taken over those values."""
     D = 64
-    for q, top in ((4, D * 16 - 1), (0, D - 1), (8, D * 256 - 1)):
-        row = np.array([[top] * 5, [top - (1 << q) // 2] * 5], np.uint16)
-        out = orc.reduce(row, 5, q, 0xFFFF, D)
-        assert out.max() <= (D - 1) * 256 + 127
-        assert ((out + 128) >> 8).max() <= D - 1
-    # untouched below the bound: 63.25 px -> 63.25 * 256
+    # reduction: the top of the range survives, 63.9375 px -> 63.9375 * 256
+    assert orc.reduce(np.array([[63 * 16 + 15] * 5], np.uint16), 5, 4, 0xFFFF, D)[0, 0] == 63 * 256 + 240
     assert orc.reduce(np.array([[63 * 16 + 4] * 5], np.uint16), 5, 4, 0xFFFF, D)[0, 0] == 63 * 256 + 64
+    # the 16-bit limit: only at D = 256 with 8 fractional bits (0xFFFF = invalid)
+    assert orc.reduce(np.array([[65535] * 5], np.uint16), 5, 8, 0, 256)[0, 0] == 0xFFFE
+    m = orc.Model(h=4, D=D, q=11, sigma=(1.0, 1.0, 100.0), alpha=0.0, horizon_row=0.0)
+    top, edge = 63 * 256 + 240, 63 * 256 + 127             # 63.9375 px and D - 1/2 - 1/256
+    # ground / sky: Eq. 4 of d' itself (sigma_S = 100 keeps it in the Gaussian branch)
+    assert orc.cost_sky(m, top) > orc.cost_sky(m, edge)
+    # object: pixel index D - 1 (the clamped value rounds to 63), not 64
+    assert orc.cost_object(m, top, 63) == orc.cost_object(m, edge, 63) == orc.cost_object(m, 63 * 256, 63)
+    # span mean over the clamped values: {63.9375, 61.1} -> {63.496, 61.1}: mean 62.30 -> 62,
+    # where the unclamped mean 62.52 would round to 63
+    col = np.array([top, 61 * 256 + 26, -1, -1], np.int32)
+    assert orc.span_mean(m, col, 0, 1) == 62
+    assert orc.span_mean(m, np.array([top, top, -1, -1], np.int32), 0, 1) == 63
 
 
 def test_reduce_properties():
@@ -144,8 +155,9 @@ def test_reduce_properties():
 
 
 def test_span_mean_exact_half_up():
-    """f_n rounded half up in exact arithmetic (L#10), clamp to D-1,
-    no valid pixel -> 0 (L#11); checked against Python Fractions."""
+    """f_n rounded half up in exact arithmetic (L#10) over the object
+    disparities (each pixel clamped below D - 1/2, L#27, so f <= D - 1), no valid
+    pixel -> 0 (L#11); checked against Python Fractions."""
     rng = np.random.default_rng(5)
     m = _model(h=40, D=16)
     for _ in range(300):
@@ -154,14 +166,15 @@ def test_span_mean_exact_half_up():
         # force exact .5 ties often
         col[rng.random(40) < 0.3] = rng.integers(0, 16) * 256 + 128
         vb = int(rng.integers(0, 40)); vt = int(rng.integers(vb, 40))
-        vals = [int(x) for x in col[vb:vt + 1] if x >= 0]
+        vals = [min(int(x), 15 * 256 + 127) for x in col[vb:vt + 1] if x >= 0]
         if not vals:
             want = 0
         else:
-            want = min(15, math.floor(Fraction(sum(vals), 256 * len(vals)) + Fraction(1, 2)))
+            want = math.floor(Fraction(sum(vals), 256 * len(vals)) + Fraction(1, 2))
+            assert want <= 15
         assert orc.span_mean(m, col, vb, vt) == want
     col = np.full(5, 15 * 256 + 200, np.int32)
-    assert orc.span_mean(m, col, 0, 4) == 15                 # 15.78 -> 16 -> clamp 15
+    assert orc.span_mean(m, col, 0, 4) == 15                 # 15.78 -> object 15.496 -> 15
 
 
 def test_stixel_data_is_sum_of_pixel_costs():

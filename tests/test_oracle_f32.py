@@ -24,7 +24,7 @@ def test_f32_invalid_cases():
     for bad in (np.nan, np.inf, -np.inf, -0.25, 64.0, 100.0):
         assert _one([bad, 10.0], D=D) == 2560           # only 10 px counts
         assert _one([bad], D=D) == -1
-    assert _one([63.99], D=D) == 63 * 256 + 127          # L#27 clamp below D - 1/2
+    assert _one([63.99], D=D) == 16381                   # floor(63.99 * 256 + 1/2), not clamped (L#27)
 
 
 def test_f32_equals_u16_on_the_sixteenth_grid():

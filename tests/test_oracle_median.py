@@ -32,8 +32,8 @@ def test_median_invalid_and_range():
     assert _one([INV, 48, INV]) == 768         # only 3 px valid
     assert _one([INV, INV]) == -1
     assert _one([128 * 16, 32], D=128) == 512  # 128 px >= D is invalid -> median of {2}
-    # 127.9375 px would round to pixel disparity 128 = D: clamped below D - 1/2 (L#27)
-    assert _one([127 * 16 + 15], D=128) == 127 * 256 + 127
+    # 127.9375 px stays (L#27: only the object model clamps below D - 1/2)
+    assert _one([127 * 16 + 15], D=128) == (127 * 16 + 15) * 16
     assert _one([127 * 16 + 7], D=128) == (127 * 16 + 7) * 16      # 127.4375 px: unchanged
 
 
@@ -44,7 +44,7 @@ def test_median_s1_is_transpose_and_equals_mean():
     a = orc.reduce(img, 1, 4, INV, 128, mode=1)
     b = orc.reduce(img, 1, 4, INV, 128, mode=0)
     assert (a == b).all()
-    want = np.minimum(img.T[:, ::-1].astype(np.int64) * 16, 127 * 256 + 127)   # L#27 clamp
+    want = img.T[:, ::-1].astype(np.int64) * 16                     # not clamped (L#27)
     assert (a == np.where(img.T[:, ::-1] == INV, -1, want)).all()
 
 
@@ -64,5 +64,5 @@ def test_median_matches_numpy_median():
                 if len(seg):
                     med = Fraction(int(round(2 * np.median(seg))), 2)     # exact: half-integers
                     x = med * 256 / (1 << q)
-                    want = min(int((x + Fraction(1, 2)).__floor__()), (D - 1) * 256 + 127)
+                    want = int((x + Fraction(1, 2)).__floor__())          # not clamped (L#27)
                 assert got[c, H - 1 - r] == want, (s, q, c, r, seg)

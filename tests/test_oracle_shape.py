@@ -43,13 +43,18 @@ def test_complexity_shape():
         c[rng.random((n, h)) < 0.05] = -1
         return c
 
-    hs = [96, 192, 384]
-    th = [_time_frame(orc.Model(h=h, D=D), cols_for(12, h)) for h in hs]
-    # the same 8 columns tiled, so only the column count changes
+    hs = [192, 384, 768]
     base = cols_for(8, 192)
-    ns = [8, 24, 64]
-    tn = [_time_frame(orc.Model(h=192, D=D), np.tile(base, (n // 8, 1))) for n in ns]
-    eh, en = _slope(hs, th), _slope(ns, tn)
+    ns = [16, 64, 256]
+    # wall-clock shape: measured twice (best of 7 each) so that one burst of other
+    # load on the host cannot fail the pin; both exponents must hold in one round
+    for attempt in range(2):
+        th = [_time_frame(orc.Model(h=h, D=D), cols_for(6, h), reps=7) for h in hs]
+        # the same 8 columns tiled, so only the column count changes
+        tn = [_time_frame(orc.Model(h=192, D=D), np.tile(base, (n // 8, 1)), reps=7) for n in ns]
+        eh, en = _slope(hs, th), _slope(ns, tn)
+        if 1.8 <= eh <= 2.3 and 0.9 <= en <= 1.2:
+            break
     assert 1.8 <= eh <= 2.3, (eh, th)
     assert 0.9 <= en <= 1.2, (en, tn)
 

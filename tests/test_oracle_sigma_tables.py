@@ -27,10 +27,11 @@ def test_eq4_closed_form_per_entry():
     for f in range(m.D):
         want = round(2 ** 11 * (math.log(m.sigma_o_f[f] * math.sqrt(2 * math.pi)) - math.log(0.85)))
         assert orc.cost_object(m, 256 * f, f) == want
-        # one disparity off: + 1 / (2 sigma_f^2), unless capped
+        # one disparity off: + 1 / (2 sigma_f^2), unless capped (pixels stay below D, L#23)
         x = math.log(m.sigma_o_f[f] * math.sqrt(2 * math.pi)) - math.log(0.85) + 1 / (2 * m.sigma_o_f[f] ** 2)
         cap = math.log(m.D) - math.log(0.15)
-        assert orc.cost_object(m, 256 * (f + 1), f) == round(2 ** 11 * min(x, cap))
+        g = f + 1 if f + 1 < m.D else f - 1
+        assert orc.cost_object(m, 256 * g, f) == round(2 ** 11 * min(x, cap))
     for v in range(m.h):
         dg = orc.ground_R(m, v)
         want = round(2 ** 11 * (math.log(m.sigma_g_v[v] * math.sqrt(2 * math.pi)) - math.log(0.85)))
