@@ -1,8 +1,10 @@
 #!/usr/bin/env python3
 """Small end-to-end run of the CUDA path for compute-sanitizer (memcheck /
 racecheck / synccheck): a few columns of C1/C2-like frames in exact mode,
-mean and median reductions, the f2 tables, D = 256, and a
-dense-ring (wide band) model; each result checked against the oracle."""
+mean and median reductions (the row-wise register reduction on 16-byte aligned
+frames, the tiled one otherwise), the f2 tables, D = 256, a dense-ring (wide
+band) model and top-of-range pixels (L#27), each under both DP launch plans (4
+and 8 warps per column); each result checked against the oracle."""
 import os
 import sys
 
@@ -29,11 +31,15 @@ cases.append(("f2", mp.make(max_disparity=D, ground_slope=0.5,
                             sigma_ground_v=rng.uniform(0.8, 3.0, H).astype(np.float32)), fr))
 cases.append(("d256", mp.make(max_disparity=256, ground_slope=1.5),
               np.stack([synth.uniform_random_image(3, 30, 70, 256)])))
+ft = rng.integers(62 << 4, 64 << 4, size=(1, 48, 1024)).astype(np.uint16)   # top of range, tight rows
+cases.append(("top", mp.make(max_disparity=64, ground_slope=0.6), ft))
+cases.append(("ragged", mp.make(max_disparity=D, ground_slope=0.5), np.ascontiguousarray(fr[:, :, :37])))
 bad = 0
 for name, p, frames in cases:
-    g, gc, _, hd = run_gpu(p, frames)
     o, oc = run_oracle(p, frames)
-    nb = len(compare_exact(g, gc, o, oc, p["cost_frac_bits"]))
-    bad += nb
-    print(f"{name}: {len(g[0])} columns, mismatches {nb}")
+    for plan in (4, 8):
+        g, gc, _, hd = run_gpu(p, frames, plan=plan)
+        nb = len(compare_exact(g, gc, o, oc, p["cost_frac_bits"]))
+        bad += nb
+        print(f"{name} (plan {plan}): {len(g[0])} columns, mismatches {nb}")
 sys.exit(1 if bad else 0)
