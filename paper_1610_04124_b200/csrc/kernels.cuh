@@ -1227,25 +1227,12 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
           int afI = argf;
           int prevCO = __shfl_sync(0xffffffffu, bI, 0);
           int prevF = __shfl_sync(0xffffffffu, argf, 0);
-          int rB = __shfl_sync(0xffffffffu, bI, 1);
-          int rF = __shfl_sync(0xffffffffu, argf, 1);
           int off = 0;                                  // tri_off(jp)
           STX_STAMP(b, 21);
           for (int jp = 0; jp < jn; ++jp) {
             const int2 q = pq[jp + 1];
-            const int4 dcell = cl[off];                 // diagonal cell (bottom j, target j)
-            const int dc = min(dcell.x + prevCO + ((dcell.w > prevF) ? oh : ol), dcell.y + prevCG);
-            const bool take = dc < rB;
-            const int COj = take ? dc : rB;
-            const int Fj = take ? dcell.z : rF;
-            // latency plan: the next target's running minimum over bottoms < j comes
-            // from its lane BEFORE this step's update, and its cell at bottom j is
-            // evaluated here redundantly, so the shuffle leaves the loop-carried chain
-            int pB = 0, pF = 0;
-            if constexpr (CW == 8) {
-              pB = __shfl_sync(0xffffffffu, bI, (jp + 2) & 31);
-              pF = __shfl_sync(0xffffffffu, afI, (jp + 2) & 31);
-            }
+            // every lane's cell (bottom j, target K0 + lane); lane jp + 1's is the
+            // diagonal, so after the update that lane holds C_O[j] and its f
             {
               const int4 lc = cl[off + lane - jp - 1];  // (lanes <= jp read a dead slot)
               const int cand = min(lc.x + prevCO + ((lc.w > prevF) ? oh : ol), lc.y + prevCG);
@@ -1253,16 +1240,8 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
               bI = upd ? cand : bI;
               afI = upd ? lc.z : afI;
             }
-            if constexpr (CW == 8) {
-              const int4 nc = cl[min(off + 1, kTri - 1)];  // cell (bottom j, target j + 1)
-              const int nd = min(nc.x + prevCO + ((nc.w > prevF) ? oh : ol), nc.y + prevCG);
-              const bool nt = nd < pB;                      // same rule as the lane's update
-              rB = nt ? nd : pB;
-              rF = nt ? nc.z : pF;
-            } else {
-              rB = __shfl_sync(0xffffffffu, bI, (jp + 2) & 31);
-              rF = __shfl_sync(0xffffffffu, afI, (jp + 2) & 31);
-            }
+            const int COj = __shfl_sync(0xffffffffu, bI, jp + 1);
+            const int Fj = __shfl_sync(0xffffffffu, afI, jp + 1);
             mgI = min(mgI, prevCO + q.x);               // ground chain (value only)
             prevCG = q.y + mgI;
             prevCO = min(COj & ~31, kChainBig);
