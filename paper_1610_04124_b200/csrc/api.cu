@@ -589,7 +589,13 @@ static int launch_reduce(stixels_handle* h, const void* d_disp, int64_t pitch, i
   if (r.vec && (r.s == 3 || r.s == 5 || r.s == 7 || r.s == 10)) {
     auto go_rr = [&](auto kern, int G) {
       const int ngroups = (h->n_cols + G - 1) / G;
-      dim3 g((ngroups + kRRGroups - 1) / kRRGroups, (h->H + 32 * kRRWarps - 1) / (32 * kRRWarps), batch);
+      const int rows_blocks = (h->H + 32 * kRRWarps - 1) / (32 * kRRWarps);
+      // full batches: 8 groups per warp (loads of the next group in flight); a
+      // batch of a few frames: one group per warp, so the grid covers the SMs and
+      // the latency is one span's round trip (BASELINE configs[1])
+      r.rr_groups = ((long)batch * rows_blocks * ((ngroups + kRRGroups - 1) / kRRGroups) >= 4L * h->sms)
+                        ? kRRGroups : 1;
+      dim3 g((ngroups + r.rr_groups - 1) / r.rr_groups, rows_blocks, batch);
       kern<<<g, 32 * kRRWarps, 0, s>>>(r);
     };
 #define STX_RR(BPPV, SWV)                                                                        \
@@ -646,7 +652,20 @@ static int launch_dp(stixels_handle* h, const uint16_t* d_cols, int batch, stixe
   const int smem = A.shared_bytes + C * A.col_bytes;
   int grid = std::min(h->grid, (A.items + C - 1) / C);
   const int threads = C * cw * 32;
-  auto go = [&](auto kern) { kern<<<grid, threads, smem, s>>>(A); };
+  // launched with programmatic stream serialisation: its CTA-table setup may
+  // overlap the preceding reduction; it waits (griddepcontrol.wait) before
+  // reading the reduced columns
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  auto go = [&](auto kern) { cudaLaunchKernelEx(&cfg, kern, A); };
   dispatch_dp(h, cw, go);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(h, STIXELS_ERR_CUDA, std::string("dp_kernel: ") + cudaGetErrorString(e));

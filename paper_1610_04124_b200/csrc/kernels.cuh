@@ -45,6 +45,7 @@ struct ReduceArgs {
   int W, H, n_cols, s, tc, q_bits, D, bpp;
   int w2;               // tile row stride in 32-bit words (odd)
   int vec;              // 16-byte loads allowed (base and pitch 16-byte aligned)
+  int rr_groups;        // reduce_rows_kernel: column groups walked per warp
   uint32_t invalid;
   uint16_t* out;        // [batch][n_cols][H], 0xFFFF = invalid
 };
@@ -57,6 +58,7 @@ __host__ __device__ inline int red_tile_words(int tc, int s, int bpp) {
 // SW > 0: the stixel width as a compile-time constant (the headline s = 5), 0: a.s
 template <bool MEDIAN, int BPP, int SW>
 __global__ void __launch_bounds__(kRedThreads) reduce_kernel(ReduceArgs a) {
+  asm volatile("griddepcontrol.launch_dependents;");   // the DP kernel may start its setup
   const int sw = SW > 0 ? SW : a.s;
   extern __shared__ uint32_t tile32[];           // [kRedRows][w2] raw input bytes
   // floor(x / d) for d = 2n <= 2 kMedianMaxS... via a multiply-high by floor(2^32/d)
@@ -209,10 +211,11 @@ struct RowRed {
 };
 constexpr int kRRWarps = 8;                              // warps (column groups) per CTA
 
-constexpr int kRRGroups = 8;                             // column groups per warp (loop)
+constexpr int kRRGroups = 8;                             // column groups per warp (loop), full batches
 
 template <bool MEDIAN, int BPP, int SW>
 __global__ void __launch_bounds__(32 * kRRWarps, 4) reduce_rows_kernel(ReduceArgs a) {
+  asm volatile("griddepcontrol.launch_dependents;");   // the DP kernel may start its setup
   using RR = RowRed<BPP, SW>;
   constexpr int G = RR::G, NV = RR::NV;
   __shared__ uint32_t rcp[2 * SW + 2];
@@ -223,8 +226,8 @@ __global__ void __launch_bounds__(32 * kRRWarps, 4) reduce_rows_kernel(ReduceArg
   const int r = (blockIdx.y * kRRWarps + (threadIdx.x >> 5)) * 32 + lane;   // image row
   const int frame = blockIdx.z;
   if (r >= a.H) return;
-  const int cg0 = blockIdx.x * kRRGroups;
-  const int cg1 = min(cg0 + kRRGroups, (a.n_cols + G - 1) / G);
+  const int cg0 = blockIdx.x * a.rr_groups;
+  const int cg1 = min(cg0 + a.rr_groups, (a.n_cols + G - 1) / G);
   const uint8_t* row = a.disp + ((int64_t)frame * a.H + r) * a.pitch;
   const uint32_t lim = (uint32_t)a.D << a.q_bits;
   const int shift = kRBits + 1 - a.q_bits;
@@ -689,6 +692,9 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
       tri_jk[tri_off(jp) + kp - jp - 1] = (uint16_t)(jp | (kp << 8));
   __syncthreads();
   const uint8_t* Eb = reinterpret_cast<const uint8_t*>(E);
+  // programmatic dependent launch: everything above (CTA tables) overlaps the
+  // reduction kernel's tail; the reduced columns are read only after this wait
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 
   ColSmem cs = carve<DP, SPARSE, CW>(smem + a.shared_bytes + cslot * a.col_bytes, h);
   // {T[j], N4[j]} of row j: the first 8 bytes of the record's second half
