@@ -14,7 +14,7 @@ src = open(os.path.join(os.path.dirname(__file__), "..", "paper_1610_04124_b200"
 marks = [("auto rect_run", "rect_run"), ("auto merge_part", "merge_part"), ("auto bulk_chunks", "bulk_chunks"),
          ("prologue A", "prologue"), ("auto build_priv", "build_priv"), ("auto precompute_cells", "precompute"),
          ("auto copy_seed", "copy_seed"), ("block 0 has only", "block0"), ("for (int b = 0; b < nb; ++b)", "block-serial"),
-         ("for (int jp = 0; jp < jn; ++jp)", "chain"), ("STX_STAMP(b, 14)", "block-serial"),
+         ("for (int jp = 0; jp < jn; ++jp)", "chain"), ("STX_STAMP(b, 22)", "block-serial"),
          ("all warps: block b+1", "block-rect"), ("backtracking (P:159)", "backtrack")]
 starts = []
 for i, l in enumerate(src, 1):

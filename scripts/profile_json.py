@@ -32,7 +32,7 @@ pipe = {
     "smem_wavefronts_pct": g("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed"),
 }
 d = {"source": f"ncu --set full --clock-control none, dp_kernel launch of bench.py --batch {frames} "
-               f"(round 1, {tag})",
+               f"({tag})",
      "frames_per_launch": frames, "dram_bytes_read": rd, "dram_bytes_write": wr,
      "dram_bytes_per_frame": (rd + wr) / frames, "duration_ms_under_ncu": g("gpu__time_duration.sum"),
      "warp_instructions": g("smsp__inst_executed.sum"), "pipe_util": pipe}
