@@ -50,7 +50,8 @@ def parse():
     ap.add_argument("--weak", action="store_true",
                     help="weak scaling: every rank runs its own --batch frames")
     ap.add_argument("--distinct", type=int, default=128, help="distinct seeded frames in the pool")
-    ap.add_argument("--e2e-batch", type=int, default=1024, help="frames per e2e call (whole job)")
+    ap.add_argument("--e2e-batch", type=int, default=4096,
+                    help="frames per e2e call (whole job; default: the configs[2] step, 4096)")
     ap.add_argument("--e2e-seconds", type=float, default=1.0, help="minimum e2e timed span")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")

@@ -761,8 +761,11 @@ int stixels_compute_host(stixels_handle* h, const void* h_disp, int64_t pitch, i
   CU(cudaStreamWaitEvent(h->hs[0], h->ev_entry, 0), h);
   CU(cudaStreamWaitEvent(h->hs[1], h->ev_entry, 0), h);
   int launches = 0;
-  for (int b0 = 0, it = 0; b0 < batch; b0 += chunk, ++it) {
-    const int nb = std::min(chunk, batch - b0);
+  // the first stage is small (a quarter) so that compute starts after a short
+  // copy; the rest are full stages
+  const int first = std::max(1, chunk / 4);
+  for (int b0 = 0, it = 0, nb = 0; b0 < batch; b0 += nb, ++it) {
+    nb = std::min(it == 0 ? first : chunk, batch - b0);
     const int i = it & 1;
     cudaStream_t s = h->hs[i];
     const size_t items = (size_t)nb * h->n_cols;
