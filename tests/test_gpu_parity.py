@@ -530,3 +530,20 @@ def test_top_of_range_pixels_exact(D, q):
     p = mp.make(max_disparity=D, disp_frac_bits=q, invalid_value=0xFFFF if q < 8 else 0,
                 ground_slope=D / (2.0 * H), cost_frac_bits=10 if D > 128 else 11)
     _assert_exact(p, f)
+
+
+def test_launch_plan_api():
+    """stixels_set_launch_plan / stixels_query_launch: the shape is 0 before the
+    first launch, a forced plan is reported back, other values are ARG errors."""
+    from paper_1610_04124_b200 import stixels as S
+    frames = _frames_c2(1, seed0=2200, W=320, H=120)
+    p = mp.make()
+    hd = S.Handle(S.params_from_dict(p, 120), 320, 120, 1)
+    assert hd.last_launch_shape() == (0, 0)
+    for bad in (1, 5, 16, -4):
+        with pytest.raises(S.StixelsError):
+            hd.set_launch_plan(bad)
+    hd.destroy()
+    for plan in (4, 8):
+        _, _, _, h2 = run_gpu(p, frames, plan=plan)
+        assert h2.last_launch_shape()[0] == plan
