@@ -338,14 +338,18 @@ __global__ void __launch_bounds__(32 * kRRWarps, 4) reduce_rows_kernel(ReduceArg
 // registers with warp shuffles; it also finalises each target -- ground and sky
 // running minima (their data term does not depend on the predecessor, so
 // GR^k = PG[k+1] + min_j (C_O[j-1] + t - PG[j])), the index table and the
-// 32-byte record of row k+1 that later rectangles read.  Meanwhile warp 1 builds
-// block b+1's priv rows and warps 1-3 (the "rectangle" warps) evaluate every
-// cell of block b+1's targets whose bottom is already final (j <= K0), in 32-row
-// chunks handed out dynamically; warp 0 joins them after its triangle.  Only the
-// newest chunk (bottoms of block b) waits for warp 0: warps 0-1 take 16 rows
-// each while warps 2-3 precompute block b+1's triangle cells.
-// Exact mode (L#22): all costs are integer quanta < 2^24 carried in fp32, so
-// adds/mins are exact and every decision matches the oracle.
+// 32-byte record of row k+1 that later rectangles read (the candidate prior as a
+// step function of the object mean f).  Meanwhile warps 1-2 build block b+1's
+// priv rows and warps 1-3 (the "rectangle" warps) evaluate every cell of block
+// b+1's targets whose bottom is already final (j <= K0), in 32-row chunks handed
+// out dynamically; warp 0 joins them after its triangle.  Only the newest chunk
+// (bottoms of block b) waits for warp 0: warps 0-1 take 16 rows each while warps
+// 2-3 precompute block b+1's triangle cells.  (Latency plan, CW = 8: 7 rectangle
+// warps, the newest chunk as 4 x 8 rows, the precompute in phase 1 into a second
+// cell buffer.)
+// Exact mode (L#22): all costs are integer quanta < 2^24 (int32 x 32 in the
+// IW rectangle and chain, integer-valued fp32 elsewhere), so adds and mins are
+// exact and every decision matches the oracle.
 // ---------------------------------------------------------------------------
 constexpr int kCW = 4;                 // warps per column
 // IW scale: priv rows, W-rows and the records' predecessor terms are int32 quanta
