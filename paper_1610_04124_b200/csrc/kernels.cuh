@@ -955,20 +955,14 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
     float* tS = cs.priv + h;
     uint32_t* tD = reinterpret_cast<uint32_t*>(cs.priv + 2 * h);
     // one row v of prologue A from its reduced value dR (-1 invalid)
-    auto prologue_row = [&](int v, int dR) {
+    auto prologue_row = [&](int v, int dR, float xg, float xs) {
       const bool valid = dR >= 0;
       // the object model's view of the pixel (L#27): clamped below D - 1/2, so its
       // rounding (the pair-LUT index, L#9) and every span mean lie in [0, D);
       // ground and sky use dR itself (Eq. 4)
       const int dO = min(dR, ((a.D - 1) << kRBits) + (1 << (kRBits - 1)) - 1);
       const int dr = valid ? (dO + (1 << (kRBits - 1))) >> kRBits : -1;   // round half up (L#9)
-      if (v < h) {
-        float xg = capQ, xs = capQ;
-        if (valid) {
-          const float* gGv = PAIR2D ? a.gG + v * a.gG_stride : a.gG;   // f2: per-row tables
-          xg = __ldg(gGv + min(abs(dR - __ldg(a.dgR + v)), a.LG - 1));
-          xs = __ldg(a.gS + min(dR, a.LS - 1));
-        }
+      if (v < h) {                       // (xg, xs: the row's ground / sky cost, Eq. 4)
         tG[v] = xg; tS[v] = xs;
         tD[v] = valid ? (uint32_t)dO + (1u << (kRBits - 1)) : 0u;
       }
@@ -987,14 +981,35 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
       const uint32_t ehi = PAIR2D ? (uint32_t)(valid ? dr : a.D + 1) : (uint32_t)(dmr * 4);
       cs.eo[v] = (uint32_t)(cc * a.esz * 4 + (dmr - cc) * 4) | (ehi << 16);
     };
-    for (int v = ctid; v < h + 2; v += CW * 32) {
-      int dR = -1;
-      if (v < h) {
-        const uint32_t u = col[v];
+    // 4 rows per thread per pass, their loads issued together: the column values
+    // and ground-model entries first, then the cost-table entries they index (two
+    // memory round trips per pass instead of two per row)
+    for (int v0 = ctid; v0 < h + 2; v0 += 4 * CW * 32) {
+      int dR[4], dg[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int v = v0 + k * CW * 32;
+        const uint32_t u = v < h ? __ldg(col + v) : 0xffffu;
         // valid below D (L#23: a caller-made column value >= D * 256 is invalid)
-        dR = (u == 0xffffu || u >= ((uint32_t)a.D << kRBits)) ? -1 : (int)u;
+        dR[k] = (u == 0xffffu || u >= ((uint32_t)a.D << kRBits)) ? -1 : (int)u;
+        dg[k] = v < h ? __ldg(a.dgR + v) : 0;
       }
-      prologue_row(v, dR);
+      float xg[4], xs[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int v = v0 + k * CW * 32;
+        xg[k] = capQ; xs[k] = capQ;
+        if (dR[k] >= 0) {
+          const float* gGv = PAIR2D ? a.gG + v * a.gG_stride : a.gG;   // f2: per-row tables
+          xg[k] = __ldg(gGv + min(abs(dR[k] - dg[k]), a.LG - 1));
+          xs[k] = __ldg(a.gS + min(dR[k], a.LS - 1));
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int v = v0 + k * CW * 32;
+        if (v < h + 2) prologue_row(v, dR[k], xg[k], xs[k]);
+      }
     }
 
     for (int i = ctid; i < DP; i += CW * 32) ANg[i] = 0.f;   // W[.][0] = 0
