@@ -1018,27 +1018,30 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
     STX_STAMP(63, w);                    // clock calibration (all warps just released)
 
     // ---------------- prologue B (4 warps): prefix sums --------------
-    // warp 0: ground PG, warp 1: sky PS, warp 2: disparity T, warp 3: count N4
-    {
-      float cf = 0.f;
-      uint32_t cu = 0;
-      if (lane == 0) { if (w == 0) PGg[0] = 0.f; if (w == 1) PSg[0] = 0.f; }
-      for (int v0 = 0; v0 < (w < 4 ? h : 0); v0 += 32) {     // warps 4.. (CW = 8) idle
-        const int v = v0 + lane;
-        if (w < 2) {
-          const float x = (v < h) ? ((w == 0) ? tG[v] : tS[v]) : 0.f;
-          const float in = warp_incl_scan(x, lane) + cf;
-          if (v < h) ((w == 0) ? PGg : PSg)[v + 1] = in;
-          cf = __shfl_sync(0xffffffffu, in, 31);
-        } else {
-          const uint32_t t = (v < h) ? tD[v] : 0u;
-          const uint32_t x = (w == 2) ? t : (t ? 4u : 0u);
-          const uint32_t in = warp_incl_scan(x, lane) + cu;
-          if (v < h) {
-            if (w == 2) cs.rec[2 * (v + 1) + 1].x = in;   // T[v+1]
-            else cs.rec[2 * (v + 1) + 1].y = in;          // N4[v+1]
-          }
-          cu = __shfl_sync(0xffffffffu, in, 31);
+    // warp 0: ground PG, warp 1: sky PS, warp 2: disparity T, warp 3: count N4.
+    // Two-level: lane l sums its segment of ceil(h/32) consecutive rows, one warp
+    // scan of the 32 segment totals, then each lane writes its segment's prefixes
+    // (exact integer quanta in exact mode, so the order of the adds is immaterial).
+    if (w < 4) {                        // warps 4.. (CW = 8) idle
+      const int seg = (h + 31) >> 5;
+      const int s0 = min(lane * seg, h), s1 = min(s0 + seg, h);
+      if (w < 2) {
+        const float* src = (w == 0) ? tG : tS;
+        float* dst = (w == 0) ? PGg : PSg;
+        float tot = 0.f;
+        for (int v = s0; v < s1; ++v) tot += src[v];
+        float acc = warp_incl_scan(tot, lane) - tot;   // exclusive prefix of the totals
+        if (lane == 0) dst[0] = 0.f;
+        for (int v = s0; v < s1; ++v) { acc += src[v]; dst[v + 1] = acc; }
+      } else {
+        uint32_t tot = 0;
+        for (int v = s0; v < s1; ++v) { const uint32_t t = tD[v]; tot += (w == 2) ? t : (t ? 4u : 0u); }
+        uint32_t acc = warp_incl_scan(tot, lane) - tot;
+        for (int v = s0; v < s1; ++v) {
+          const uint32_t t = tD[v];
+          acc += (w == 2) ? t : (t ? 4u : 0u);
+          if (w == 2) cs.rec[2 * (v + 1) + 1].x = acc;   // T[v+1]
+          else cs.rec[2 * (v + 1) + 1].y = acc;          // N4[v+1]
         }
       }
       __threadfence_block();
