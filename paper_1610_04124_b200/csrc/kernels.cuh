@@ -378,7 +378,7 @@ __device__ __forceinline__ unsigned long long stx_globaltimer() {
 }
 #define STX_STAMP(blk, slot)                                                             \
   do {                                                                                   \
-    if (blockIdx.x == 0 && first_item && lane == 0 && (blk) < 64)                        \
+    if (blockIdx.x == 0 && trace_item && lane == 0 && (blk) < 64)                        \
       a.trace[(cslot * 64 + (blk)) * 32 + (slot)] = stx_globaltimer();                  \
   } while (0)
 #else
@@ -945,10 +945,11 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
   constexpr int NB = NS / 2;           // f slices per builder warp (warps 1 and 2)
   CT fr[NB];                           // builder warps: W[f][32 bt] for f = lane + 32 (c0 + c)
 
-  bool first_item = true;
-  (void)first_item;
   for (int item = slot_global; item < a.items; item += gridDim.x * a.cols_per_cta) {
     const uint16_t* col = a.cols + (int64_t)item * h;
+    // (diagnostic timeline: the group's third column, past the cold start)
+    const bool trace_item = item == slot_global + 2 * gridDim.x * a.cols_per_cta;
+    (void)trace_item;
     if (w == 0) STX_STAMP(60, 0);       // item start
     // ---------------- prologue A (all 4 warps): per-pixel costs (a3-a4) ----------
     float* tG = cs.priv;                 // temporaries in the (idle) priv rows
@@ -1017,6 +1018,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
     named_bar(bar_col, CW * 32);
     STX_STAMP(63, w);                    // clock calibration (all warps just released)
 
+    if (w == 0) STX_STAMP(60, 3);       // prologue A done
     // ---------------- prologue B (4 warps): prefix sums --------------
     // warp 0: ground PG, warp 1: sky PS, warp 2: disparity T, warp 3: count N4.
     // Two-level: lane l sums its segment of ceil(h/32) consecutive rows, one warp
@@ -1044,9 +1046,9 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
           else cs.rec[2 * (v + 1) + 1].y = acc;          // N4[v+1]
         }
       }
-      __threadfence_block();
     }
     named_bar(bar_col, CW * 32);
+    if (w == 0) STX_STAMP(60, 4);       // prologue B done
 
     // build priv W-rows of block bt and the anchor row 32(bt+1): a sequential
     // prefix over rows, per f, so the f slices are independent.  Two
@@ -1170,6 +1172,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
       build_priv(0);
     }
     named_bar(bar_col, CW * 32);
+    if (w == 0) STX_STAMP(60, 5);       // block 0's priv rows built
 
     // block 0 has only the j = 0 candidate (Eq. 5) and its triangle
     {
@@ -1508,23 +1511,21 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
       if (lastO < cost) { c = 1; cost = lastO; }
       if (lastS < cost) { c = 2; cost = lastS; }
       uint2* lst = reinterpret_cast<uint2*>(cs.priv);    // scratch (priv rows are dead)
-      float* lsd = cs.priv + 2 * h;
       int n = 0;
       if (lane == 0) {
+        // the walk reads only the index tables (shared memory); the stixels'
+        // disparities are looked up in the parallel write below
         int kb = h - 1;
         while (true) {
           int j, cp;
-          float d;
           if (c == 1) {
-            uint16_t x = cs.argO[kb]; j = x & 0xfff; cp = x >> 12; d = (float)cs.fpv[kb];
+            uint16_t x = cs.argO[kb]; j = x & 0xfff; cp = x >> 12;
           } else if (c == 0) {
             j = cs.argG[kb]; cp = j ? 1 : kStart;
-            d = (float)__ldg(a.dgR + j) * (1.0f / (1 << kRBits));
           } else {
-            uint16_t x = cs.argS[kb]; j = x & 0xfff; cp = x >> 12; d = 0.f;
+            uint16_t x = cs.argS[kb]; j = x & 0xfff; cp = x >> 12;
           }
           lst[n] = make_uint2((uint32_t)j | ((uint32_t)kb << 16), (uint32_t)c);
-          lsd[n] = d;
           ++n;
           if (j == 0 || n >= h) break;
           kb = j - 1;
@@ -1542,7 +1543,9 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
         s.top = (uint16_t)(e.x >> 16);
         s.cls = (uint8_t)e.y;
         s.pad[0] = s.pad[1] = s.pad[2] = 0;
-        s.disparity = lsd[n - 1 - i];
+        // L#19: object -> its mean f, ground -> the ground model at its bottom, sky -> 0
+        s.disparity = e.y == 1 ? (float)cs.fpv[s.top]
+                    : e.y == 0 ? (float)__ldg(a.dgR + s.bottom) * (1.0f / (1 << kRBits)) : 0.f;
         o[i] = s;
       }
       if (lane == 0) {
@@ -1553,7 +1556,6 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
       __syncwarp();
     }
     if (w == 0) STX_STAMP(60, 2);       // column written
-    first_item = false;
     named_bar(bar_col, CW * 32);
   }
 }

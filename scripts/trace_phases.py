@@ -1,5 +1,5 @@
 #!/usr/bin/env python3
-"""Phase timeline of dp_kernel's first column per column group of CTA 0 (diagnostic
+"""Phase timeline of dp_kernel's third column per column group of CTA 0 (diagnostic
 build libstixels_trace.so, -DSTX_TRACE).  Prints, per 32-row block b, cycles
 relative to the block start: serial triangle done, build done, each warp's bulk
 end, the bar release, each warp's newest-chunk end, the block end.
@@ -59,5 +59,6 @@ for g in range(4):
     it = t[g, 60]
     if it[0]:
         b0 = t[g, 0, 0]
-        print(f"  item start -> block 0 start {int(b0 - it[0])}, blocks {int(it[1] - b0)}, "
-              f"backtrack+write {int(it[2] - it[1])} cycles")
+        print(f"  item start -> block 0 start {int(b0 - it[0])} (prologue A {int(it[3] - it[0])}, "
+              f"B {int(it[4] - it[3])}, build {int(it[5] - it[4])}, block-0 cells {int(b0 - it[5])}), "
+              f"blocks {int(it[1] - b0)}, backtrack+write {int(it[2] - it[1])} cycles")
