@@ -1290,27 +1290,14 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
         float prevCG = __shfl_sync(0xffffffffu, pg1, 0) + mg;
         float prevCO = __shfl_sync(0xffffffffu, best, 0);
         int prevF = __shfl_sync(0xffffffffu, argf, 0);
-        // running minimum (over bottoms < j) of the next target to finalise
-        float rB = __shfl_sync(0xffffffffu, best, 1);
-        int rF = __shfl_sync(0xffffffffu, argf, 1);
         int off = 0;                                    // tri_off(jp)
         STX_STAMP(b, 21);                 // serial: merge + recovery + chain setup done
         for (int jp = 0; jp < jn; ++jp) {
           const int j = K0 + jp + 1;                    // bottom j; target j finalised
           const float4 q = cs.pgps[jp + 1];
-          // diagonal cell (bottom j, target j), evaluated redundantly by all lanes
-          // (data + min(aO, aG) computed as min(data + aO, (data + pen) + C_G): the
-          // same value, exactly so in exact mode (integer quanta))
-          const float4 dcell = cells_of(b)[off];
-          const float dd = dcell.x;
-          const float dg = dcell.y;
-          const int df = __float_as_int(dcell.z);
-          const float daO = prevCO + ((df > prevF + om) ? oh : ol);
-          const float dc = fminf(dd + daO, dg + prevCG);
-          const bool take = dc < rB;
-          const float COj = take ? dc : rB;
-          const int Fj = take ? df : rF;
-          // this lane's cell (bottom j, target k > j) with the same predecessors
+          // this lane's cell (bottom j, target k > j) with the same predecessors;
+          // lane jp + 1's is the diagonal (the 1-pixel stixel), so after the update
+          // that lane holds C_O[j] and its f
           {
             const int idx = off + lane - jp - 1;        // (lanes <= jp read a dead slot)
             const float4 lc = cells_of(b)[idx];
@@ -1327,8 +1314,8 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
             argf = upd ? f : argf;
             argc = upd ? (pg ? 0 : 1) : argc;
           }
-          rB = __shfl_sync(0xffffffffu, best, (jp + 2) & 31);
-          rF = __shfl_sync(0xffffffffu, argf, (jp + 2) & 31);
+          const float COj = __shfl_sync(0xffffffffu, best, jp + 1);
+          const int Fj = __shfl_sync(0xffffffffu, argf, jp + 1);
           // ground: GR^j = PG[j+1] + min(.., C_O[j-1] + t - PG[j])  (value only)
           mg = fminf(mg, prevCO + q.x);
           prevCG = q.y + mg;
