@@ -945,12 +945,74 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
   constexpr int NB = NS / 2;           // f slices per builder warp (warps 1 and 2)
   CT fr[NB];                           // builder warps: W[f][32 bt] for f = lane + 32 (c0 + c)
 
+  // ---------------- backtracking + extraction (a7), warp 0 ------------
+  // The list is staged in the W-row ring and the triangle cells (contiguous,
+  // >= 2h words), which the next item's prologue A and B leave alone.
+  auto backtrack = [&](int item, float lastO, float lastG, float lastS) {
+    {
+      int c = 0;
+      float cost = lastG;
+      if (lastO < cost) { c = 1; cost = lastO; }
+      if (lastS < cost) { c = 2; cost = lastS; }
+      uint2* lst = reinterpret_cast<uint2*>(cs.ring);
+      int n = 0;
+      if (lane == 0) {
+        // the walk reads only the index tables (shared memory); the stixels'
+        // disparities are looked up in the parallel write below
+        int kb = h - 1;
+        while (true) {
+          int j, cp;
+          if (c == 1) {
+            uint16_t x = cs.argO[kb]; j = x & 0xfff; cp = x >> 12;
+          } else if (c == 0) {
+            j = cs.argG[kb]; cp = j ? 1 : kStart;
+          } else {
+            uint16_t x = cs.argS[kb]; j = x & 0xfff; cp = x >> 12;
+          }
+          lst[n] = make_uint2((uint32_t)j | ((uint32_t)kb << 16), (uint32_t)c);
+          ++n;
+          if (j == 0 || n >= h) break;
+          kb = j - 1;
+          c = cp;
+        }
+      }
+      n = __shfl_sync(0xffffffffu, n, 0);
+      __syncwarp();
+      stixel_t* o = a.out + (int64_t)item * a.cap;
+      const int nw = min(n, a.cap);
+      for (int i = lane; i < nw; i += 32) {
+        uint2 e = lst[n - 1 - i];
+        stixel_t s;
+        s.bottom = (uint16_t)(e.x & 0xffff);
+        s.top = (uint16_t)(e.x >> 16);
+        s.cls = (uint8_t)e.y;
+        s.pad[0] = s.pad[1] = s.pad[2] = 0;
+        // L#19: object -> its mean f, ground -> the ground model at its bottom, sky -> 0
+        s.disparity = e.y == 1 ? (float)cs.fpv[s.top]
+                    : e.y == 0 ? (float)__ldg(a.dgR + s.bottom) * (1.0f / (1 << kRBits)) : 0.f;
+        o[i] = s;
+      }
+      if (lane == 0) {
+        a.count[item] = n;
+        if (a.col_cost) a.col_cost[item] = cost * a.cost_scale;
+        if (n > a.cap) atomicExch(a.overflow, 1);
+      }
+      __syncwarp();
+    }
+  };
+  int pend_item = -1;
+  float pendO = INF, pendG = INF, pendS = INF;
   for (int item = slot_global; item < a.items; item += gridDim.x * a.cols_per_cta) {
     const uint16_t* col = a.cols + (int64_t)item * h;
     // (diagnostic timeline: the group's third column, past the cold start)
     const bool trace_item = item == slot_global + 2 * gridDim.x * a.cols_per_cta;
     (void)trace_item;
     if (w == 0) STX_STAMP(60, 0);       // item start
+    if (w == 0 && pend_item >= 0) {
+      backtrack(pend_item, pendO, pendG, pendS);
+      pend_item = -1;
+    }
+    const int ctidA = ctid - 32;         // prologue A: warps 1 .. CW-1
     // ---------------- prologue A (all 4 warps): per-pixel costs (a3-a4) ----------
     float* tG = cs.priv;                 // temporaries in the (idle) priv rows
     float* tS = cs.priv + h;
@@ -985,11 +1047,11 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
     // 4 rows per thread per pass, their loads issued together: the column values
     // and ground-model entries first, then the cost-table entries they index (two
     // memory round trips per pass instead of two per row)
-    for (int v0 = ctid; v0 < h + 2; v0 += 4 * CW * 32) {
+    for (int v0 = ctidA; w > 0 && v0 < h + 2; v0 += 4 * (CW - 1) * 32) {
       int dR[4], dg[4];
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        const int v = v0 + k * CW * 32;
+        const int v = v0 + k * (CW - 1) * 32;
         const uint32_t u = v < h ? __ldg(col + v) : 0xffffu;
         // valid below D (L#23: a caller-made column value >= D * 256 is invalid)
         dR[k] = (u == 0xffffu || u >= ((uint32_t)a.D << kRBits)) ? -1 : (int)u;
@@ -998,7 +1060,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
       float xg[4], xs[4];
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        const int v = v0 + k * CW * 32;
+        const int v = v0 + k * (CW - 1) * 32;
         xg[k] = capQ; xs[k] = capQ;
         if (dR[k] >= 0) {
           const float* gGv = PAIR2D ? a.gG + v * a.gG_stride : a.gG;   // f2: per-row tables
@@ -1008,13 +1070,13 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
       }
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        const int v = v0 + k * CW * 32;
+        const int v = v0 + k * (CW - 1) * 32;
         if (v < h + 2) prologue_row(v, dR[k], xg[k], xs[k]);
       }
     }
 
-    for (int i = ctid; i < DP; i += CW * 32) ANg[i] = 0.f;   // W[.][0] = 0
-    if (ctid == 0) *cs.ctr = 0;
+    for (int i = ctidA; w > 0 && i < DP; i += (CW - 1) * 32) ANg[i] = 0.f;   // W[.][0] = 0
+    if (ctidA == 0) *cs.ctr = 0;
     named_bar(bar_col, CW * 32);
     STX_STAMP(63, w);                    // clock calibration (all warps just released)
 
@@ -1491,60 +1553,11 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
     }
 
     if (w == 0) STX_STAMP(60, 1);       // blocks done
-    // ---------------- backtracking + extraction (a7), warp 0 ------------
-    if (w == 0) {
-      int c = 0;
-      float cost = lastG;
-      if (lastO < cost) { c = 1; cost = lastO; }
-      if (lastS < cost) { c = 2; cost = lastS; }
-      uint2* lst = reinterpret_cast<uint2*>(cs.priv);    // scratch (priv rows are dead)
-      int n = 0;
-      if (lane == 0) {
-        // the walk reads only the index tables (shared memory); the stixels'
-        // disparities are looked up in the parallel write below
-        int kb = h - 1;
-        while (true) {
-          int j, cp;
-          if (c == 1) {
-            uint16_t x = cs.argO[kb]; j = x & 0xfff; cp = x >> 12;
-          } else if (c == 0) {
-            j = cs.argG[kb]; cp = j ? 1 : kStart;
-          } else {
-            uint16_t x = cs.argS[kb]; j = x & 0xfff; cp = x >> 12;
-          }
-          lst[n] = make_uint2((uint32_t)j | ((uint32_t)kb << 16), (uint32_t)c);
-          ++n;
-          if (j == 0 || n >= h) break;
-          kb = j - 1;
-          c = cp;
-        }
-      }
-      n = __shfl_sync(0xffffffffu, n, 0);
-      __syncwarp();
-      stixel_t* o = a.out + (int64_t)item * a.cap;
-      const int nw = min(n, a.cap);
-      for (int i = lane; i < nw; i += 32) {
-        uint2 e = lst[n - 1 - i];
-        stixel_t s;
-        s.bottom = (uint16_t)(e.x & 0xffff);
-        s.top = (uint16_t)(e.x >> 16);
-        s.cls = (uint8_t)e.y;
-        s.pad[0] = s.pad[1] = s.pad[2] = 0;
-        // L#19: object -> its mean f, ground -> the ground model at its bottom, sky -> 0
-        s.disparity = e.y == 1 ? (float)cs.fpv[s.top]
-                    : e.y == 0 ? (float)__ldg(a.dgR + s.bottom) * (1.0f / (1 << kRBits)) : 0.f;
-        o[i] = s;
-      }
-      if (lane == 0) {
-        a.count[item] = n;
-        if (a.col_cost) a.col_cost[item] = cost * a.cost_scale;
-        if (n > a.cap) atomicExch(a.overflow, 1);
-      }
-      __syncwarp();
-    }
-    if (w == 0) STX_STAMP(60, 2);       // column written
-    named_bar(bar_col, CW * 32);
+    // backtracking of this column: by warp 0 at the start of the next item, while
+    // the other warps run that item's prologue A
+    if (w == 0) { pend_item = item; pendO = lastO; pendG = lastG; pendS = lastS; }
   }
+  if (w == 0 && pend_item >= 0) backtrack(pend_item, pendO, pendG, pendS);
 }
 
 }  // namespace stx
