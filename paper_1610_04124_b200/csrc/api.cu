@@ -32,6 +32,7 @@ struct stixels_handle {
   bool pair2d = false;          // NEXT f2: sigma_O(f) table given
   bool iw = false;              // int32 W-rows with atomic band rounds (band <= 3, exact mode)
   int red_tc = 0, red_smem = 0, red_w2 = 0;
+  int smem_optin = 0;           // opt-in shared memory per block (reduce_strip_kernel stages)
   DPArgs args{};
   float* d_E = nullptr;
   float* d_E2 = nullptr;        // NEXT f2: [D+2][DP] 2-D pair table
@@ -470,6 +471,7 @@ int stixels_create(const stixels_params* params, int width, int height, int max_
   if (prop.major != 10) return bail(STIXELS_ERR_CUDA, "this library is built for sm_100a (B200) only");
   h->sms = prop.multiProcessorCount;
   int optin = (int)prop.sharedMemPerBlockOptin;
+  h->smem_optin = optin;
   auto kfun = [&](int cw) { return dp_kernel_ptr(h, cw); };
   auto cbytes = [&](int cw) {
     if (cw == 8)
@@ -587,8 +589,24 @@ static int launch_reduce(stixels_handle* h, const void* d_disp, int64_t pitch, i
   const bool med = h->p.reduce_mode == STIXELS_REDUCE_MEDIAN;
   // row-wise register kernel for the common widths (16-byte aligned frames)
   if (r.vec && (r.s == 3 || r.s == 5 || r.s == 7 || r.s == 10)) {
-    auto go_rr = [&](auto kern, int G) {
+    // strip kernel (TMA row streams) for full batches whose rows fit 2+ strip buffers
+    const int rowb = (h->W * r.bpp + 15) & ~15;       // bytes copied per image row
+    const int rs = rowb + (((rowb >> 4) & 1) ? 0 : 16); // smem row stride: odd multiple of 16 B
+    const int nstrips = batch * ((h->H + 31) >> 5);
+    const int stages = std::min(4, (h->smem_optin - kStripHdr - 128) / (32 * rs));
+    const bool strip = rowb <= pitch && stages >= 2 && nstrips >= 4 * h->sms;
+    auto go_rr = [&](auto kern, auto kstrip, int G) {
       const int ngroups = (h->n_cols + G - 1) / G;
+      r.batch = batch;
+      if (strip) {
+        r.tma_rs = rs; r.tma_rowb = rowb; r.tma_stages = stages;
+        const int smem = kStripHdr + stages * 32 * rs + 128;   // (+ slack: a ragged group's last loads)
+        cudaFuncSetAttribute(kstrip, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        const int per = (ngroups + 14) / 15;                // compute warps: the same number of groups each
+        const int nw = (ngroups + per - 1) / per;
+        kstrip<<<std::min(nstrips, h->sms), 32 * (nw + 1), smem, s>>>(r);   // + the copy-issuing warp
+        return;
+      }
       const int rows_blocks = (h->H + 32 * kRRWarps - 1) / (32 * kRRWarps);
       // full batches: 8 groups per warp (loads of the next group in flight); a
       // batch of a few frames: one group per warp, so the grid covers the SMs and
@@ -598,14 +616,24 @@ static int launch_reduce(stixels_handle* h, const void* d_disp, int64_t pitch, i
       dim3 g((ngroups + r.rr_groups - 1) / r.rr_groups, rows_blocks, batch);
       kern<<<g, 32 * kRRWarps, 0, s>>>(r);
     };
+    // integer input with the sentinel at or above D 2^Q (e.g. 0xFFFF): one compare per pixel
+    const bool invhi = r.bpp != 4 && r.invalid >= ((uint32_t)r.D << r.q_bits);
+#define STX_RR2(MED, BPPV, SWV, IH) \
+    go_rr(reduce_rows_kernel<MED, BPPV, SWV, IH>, reduce_strip_kernel<MED, BPPV, SWV, IH>, RowRed<BPPV, SWV>::G)
 #define STX_RR(BPPV, SWV)                                                                        \
     if (r.bpp == BPPV && r.s == SWV) {                                                            \
-      if (med) go_rr(reduce_rows_kernel<true, BPPV, SWV>, RowRed<BPPV, SWV>::G);                  \
-      else go_rr(reduce_rows_kernel<false, BPPV, SWV>, RowRed<BPPV, SWV>::G);                     \
+      if (med) {                                                                                  \
+        if (invhi && BPPV != 4) STX_RR2(true, BPPV, SWV, BPPV != 4);                              \
+        else STX_RR2(true, BPPV, SWV, false);                                                     \
+      } else {                                                                                    \
+        if (invhi && BPPV != 4) STX_RR2(false, BPPV, SWV, BPPV != 4);                             \
+        else STX_RR2(false, BPPV, SWV, false);                                                    \
+      }                                                                                           \
     }
     STX_RR(2, 5) else STX_RR(2, 3) else STX_RR(2, 7) else STX_RR(2, 10)
     else STX_RR(1, 5) else STX_RR(1, 3) else STX_RR(1, 7) else STX_RR(1, 10)
     else STX_RR(4, 5) else STX_RR(4, 3) else STX_RR(4, 7) else STX_RR(4, 10)
+#undef STX_RR2
 #undef STX_RR
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(h, STIXELS_ERR_CUDA, std::string("reduce_rows_kernel: ") + cudaGetErrorString(e));

@@ -46,6 +46,9 @@ struct ReduceArgs {
   int w2;               // tile row stride in 32-bit words (odd)
   int vec;              // 16-byte loads allowed (base and pitch 16-byte aligned)
   int rr_groups;        // reduce_rows_kernel: column groups walked per warp
+  int batch;            // frames in this launch
+  int tma_rs, tma_rowb; // reduce_strip_kernel: smem row stride (16 x odd bytes), bytes copied per row
+  int tma_stages;       // reduce_strip_kernel: strip buffers in flight
   uint32_t invalid;
   uint16_t* out;        // [batch][n_cols][H], 0xFFFF = invalid
 };
@@ -213,14 +216,103 @@ constexpr int kRRWarps = 8;                              // warps (column groups
 
 constexpr int kRRGroups = 8;                             // column groups per warp (loop), full batches
 
-template <bool MEDIAN, int BPP, int SW>
+// One span of G reduced columns (NV 16-byte words of one image row in registers)
+// -> G reduced values of that row, written at out[g H]: decode and validity
+// (L#23/L#28), the mean or median (L#24) of the valid pixels, half-up
+// rounding to 1/256 (the 16-bit code 0xFFFF = invalid, top value 0xFFFE, L#27).
+// The rounding division floor(num / d), d = 2n <= 2 SW, is a multiply-high by
+// rcp[d] = ceil(2^32 / d), exact without a correction step: every valid pixel is
+// below D 2^Q (integers) or D 256 (f32), so num < SW D 2^9 + SW < 2^21 and the
+// error num (rcp[d] - 2^32/d) / 2^32 < 2^-11 stays below the gap 1/d to the next
+// integer.  INVHI: the sentinel lies at or above D 2^Q, so a pixel is valid iff
+// u < D 2^Q (one compare and one predicated add per pixel).  FULL: all G columns
+// of the span exist (no per-column bound test).
+template <int SW>
+__device__ __forceinline__ void rr_rcp_init(uint32_t* rcp) {
+  for (int i = threadIdx.x; i < 2 * SW + 2; i += blockDim.x)
+    rcp[i] = i < 2 ? 0u : (uint32_t)(((1ull << 32) + (unsigned)i - 1) / (unsigned)i);
+}
+__device__ __forceinline__ void add_if_below(uint32_t& sn, uint32_t t, uint32_t lim) {
+  // sn += t if t < lim (one compare, one predicated add)
+  asm("{\n .reg .pred p;\n setp.lt.u32 p, %1, %2;\n @p add.u32 %0, %0, %1;\n}" : "+r"(sn) : "r"(t), "r"(lim));
+}
+template <bool MEDIAN, int BPP, int SW, bool INVHI, int NV, bool FULL>
+__device__ __forceinline__ void rr_reduce_span(const uint32_t (&cur)[NV * 4], int c0, int n_cols,
+                                               uint16_t* out, int H, const uint32_t* rcp, uint32_t lim,
+                                               int shift, float Df, bool inv_hi, uint32_t invalid) {
+  constexpr int G = NV * 16 / (SW * BPP);
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    if (!FULL && c0 + g >= n_cols) break;
+    uint32_t u[SW];
+    bool ok[SW];
+    // sum and count of the valid pixels packed in one word: count in bits 24..,
+    // sum (< SW 2^17 <= 2^21 for SW <= 16) below
+    uint32_t sn = 0;
+#pragma unroll
+    for (int x = 0; x < SW; ++x) {
+      const int e = g * SW + x;                        // pixel index in the span
+      const uint32_t w = cur[(e * BPP) >> 2];
+      if constexpr (BPP == 4) {
+        const float d = __uint_as_float(w);
+        ok[x] = d >= 0.f && d < Df;                    // false for NaN and +-inf too
+        u[x] = ok[x] ? (uint32_t)__float2int_rd(d * 256.f + 0.5f) : 0u;   // L#28
+        if (ok[x]) sn += u[x] + (1u << 24);
+      } else {
+        u[x] = BPP == 2 ? ((w >> (8 * ((e * 2) & 3))) & 0xffffu) : ((w >> (8 * (e & 3))) & 0xffu);
+        // (the sentinel test is redundant when it is >= the range limit)
+        if constexpr (INVHI) {
+          ok[x] = u[x] < lim;
+          if constexpr (!MEDIAN) {
+            // t = u + 2^24 in one byte permute (pixel bytes, then 0x00, 0x01)
+            const uint32_t t = BPP == 2 ? __byte_perm(w, 0x01000000u, ((e * 2) & 3) ? 0x7432u : 0x7410u)
+                                        : __byte_perm(w, 0x01000000u, 0x7440u | (uint32_t)(e & 3));
+            add_if_below(sn, t, lim + (1u << 24));
+          } else if (ok[x]) {
+            sn += u[x] + (1u << 24);
+          }
+        } else {
+          ok[x] = (inv_hi || u[x] != invalid) && (u[x] < lim);
+          if (ok[x]) sn += u[x] + (1u << 24);
+        }
+      }
+    }
+    uint32_t sum = sn & 0xffffffu, n = sn >> 24;
+    if (MEDIAN && n) {
+      const uint32_t k1 = (n - 1) >> 1, k2 = n >> 1;
+      uint32_t va = 0, vb = 0;
+#pragma unroll
+      for (int x = 0; x < SW; ++x) {
+        uint32_t less = 0, leq = 0;
+#pragma unroll
+        for (int y = 0; y < SW; ++y) {
+          less += (ok[y] && u[y] < u[x]) ? 1u : 0u;
+          leq += (ok[y] && u[y] <= u[x]) ? 1u : 0u;
+        }
+        if (ok[x] && less <= k1 && k1 < leq) va = u[x];
+        if (ok[x] && less <= k2 && k2 < leq) vb = u[x];
+      }
+      sum = va + vb;
+      n = 2;
+    }
+    // n = 0 is replaced by the invalid code
+    const uint32_t q = __umulhi((sum << shift) + n, rcp[2 * n]);
+    // (0xFFFF = invalid; the top value 65535 is stored as 0xFFFE, L#27)
+    out[g * H] = n ? (uint16_t)min(q, 0xFFFEu) : (uint16_t)0xFFFF;
+  }
+}
+
+// INVHI (integer input whose invalid sentinel lies at or above the range limit
+// D 2^Q, e.g. 0xFFFF): a pixel is valid iff u < D 2^Q, one compare; the valid
+// sum and count then take one predicated add per pixel (round 2: ~62 -> ~30
+// lane-instructions per output value).
+template <bool MEDIAN, int BPP, int SW, bool INVHI>
 __global__ void __launch_bounds__(32 * kRRWarps, 4) reduce_rows_kernel(ReduceArgs a) {
   asm volatile("griddepcontrol.launch_dependents;");   // the DP kernel may start its setup
   using RR = RowRed<BPP, SW>;
   constexpr int G = RR::G, NV = RR::NV;
   __shared__ uint32_t rcp[2 * SW + 2];
-  for (int i = threadIdx.x; i < 2 * SW + 2; i += blockDim.x)
-    rcp[i] = i < 2 ? 0u : (uint32_t)((1ull << 32) / (unsigned)i);
+  rr_rcp_init<SW>(rcp);
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int r = (blockIdx.y * kRRWarps + (threadIdx.x >> 5)) * 32 + lane;   // image row
@@ -233,7 +325,7 @@ __global__ void __launch_bounds__(32 * kRRWarps, 4) reduce_rows_kernel(ReduceArg
   const int shift = kRBits + 1 - a.q_bits;
   const float Df = (float)a.D;
   const int v = a.H - 1 - r;
-  const bool inv_hi = a.invalid >= lim;
+  const bool inv_hi = INVHI || a.invalid >= lim;
   // the span of column group cg into registers: NV vector loads, or element loads
   // within [0, W bpp) when it would overrun the row's pitch
   auto load_span = [&](int cg, uint32_t (&wv)[NV * 4]) {
@@ -260,64 +352,146 @@ __global__ void __launch_bounds__(32 * kRRWarps, 4) reduce_rows_kernel(ReduceArg
       }
     }
   };
-  uint32_t cur[NV * 4], nxt[NV * 4];
-  if (cg0 < cg1) load_span(cg0, cur);
-  for (int cg = cg0; cg < cg1; ++cg) {
-    if (cg + 1 < cg1) load_span(cg + 1, nxt);         // prefetch: loads stay in flight
-    const int c0 = cg * G;
-    uint16_t* out = a.out + ((int64_t)frame * a.n_cols + c0) * a.H + v;
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-      if (c0 + g >= a.n_cols) break;
-      uint32_t u[SW];
-      bool ok[SW];
-      // sum and count of the valid pixels packed in one word: count in bits 24..,
-      // sum (< SW 2^17 <= 2^21 for SW <= 16) below
-      uint32_t sn = 0;
-#pragma unroll
-      for (int x = 0; x < SW; ++x) {
-        const int e = g * SW + x;                        // pixel index in the span
-        const uint32_t w = cur[(e * BPP) >> 2];
-        if constexpr (BPP == 4) {
-          const float d = __uint_as_float(w);
-          ok[x] = d >= 0.f && d < Df;                    // false for NaN and +-inf too
-          u[x] = ok[x] ? (uint32_t)__float2int_rd(d * 256.f + 0.5f) : 0u;   // L#28
-        } else {
-          u[x] = BPP == 2 ? ((w >> (8 * ((e * 2) & 3))) & 0xffffu) : ((w >> (8 * (e & 3))) & 0xffu);
-          // (the sentinel test is redundant when it is >= the range limit)
-          ok[x] = (inv_hi || u[x] != a.invalid) && (u[x] < lim);
-        }
-        sn += ok[x] ? u[x] + (1u << 24) : 0u;
-      }
-      uint32_t sum = sn & 0xffffffu, n = sn >> 24;
-      if (MEDIAN && n) {
-        const uint32_t k1 = (n - 1) >> 1, k2 = n >> 1;
-        uint32_t va = 0, vb = 0;
-#pragma unroll
-        for (int x = 0; x < SW; ++x) {
-          uint32_t less = 0, leq = 0;
-#pragma unroll
-          for (int y = 0; y < SW; ++y) {
-            less += (ok[y] && u[y] < u[x]) ? 1u : 0u;
-            leq += (ok[y] && u[y] <= u[x]) ? 1u : 0u;
-          }
-          if (ok[x] && less <= k1 && k1 < leq) va = u[x];
-          if (ok[x] && less <= k2 && k2 < leq) vb = u[x];
-        }
-        sum = va + vb;
-        n = 2;
-      }
-      uint16_t val = 0xFFFF;
-      if (n) {
-        const uint32_t num = (sum << shift) + n, d = 2u * n;   // num < 2^32: sum < SW 2^16
-        uint32_t q = __umulhi(num, rcp[d]);
-        if (num - q * d >= d) ++q;                        // floor(2^32/d) under-estimates by <= 1
-        val = (uint16_t)min(q, 0xFFFEu);                   // (0xFFFF = invalid, L#27)
-      }
-      out[(int64_t)g * a.H] = val;
+  auto reduce_span = [&](const uint32_t (&cur)[NV * 4], int cg) {
+    uint16_t* o = a.out + ((int64_t)frame * a.n_cols + cg * G) * a.H + v;
+    if ((cg + 1) * G <= a.n_cols)
+      rr_reduce_span<MEDIAN, BPP, SW, INVHI, NV, true>(cur, cg * G, a.n_cols, o, a.H, rcp, lim, shift, Df, inv_hi, a.invalid);
+    else
+      rr_reduce_span<MEDIAN, BPP, SW, INVHI, NV, false>(cur, cg * G, a.n_cols, o, a.H, rcp, lim, shift, Df, inv_hi, a.invalid);
+  };
+  // two span buffers in turn (no register copies): the next group's loads stay in
+  // flight while the current one is reduced
+  uint32_t bA[NV * 4], bB[NV * 4];
+  int cg = cg0;
+  if (cg < cg1) load_span(cg, bA);
+  while (cg < cg1) {
+    if (cg + 1 < cg1) load_span(cg + 1, bB);
+    reduce_span(bA, cg);
+    if (++cg >= cg1) break;
+    if (cg + 1 < cg1) load_span(cg + 1, bA);
+    reduce_span(bB, cg);
+    ++cg;
+  }
+}
+
+
+// ---------------------------------------------------------------------------
+// K1 (strip variant, full batches): a persistent CTA per SM streams 32-row strips
+// of a frame (whole image rows, W bpp bytes each) into shared memory with
+// one-dimensional bulk copies (cp.async.bulk, the TMA engine; completion on an
+// mbarrier per buffer), kTmaStages strips in flight, so DRAM sees whole-row
+// requests.  Warps then reduce the strip exactly as reduce_rows_kernel does (lane
+// = image row, NV 16-byte shared loads per column group, rr_reduce_span): the
+// smem row stride is an odd multiple of 16 bytes, so the 8 rows a quarter-warp
+// reads sit in distinct bank groups.  A producer warp refills a buffer once every
+// compute warp has arrived on its `empty` mbarrier (no CTA-wide barrier).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void mbar_init(uint32_t a, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t a, uint32_t tx) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(tx) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      " .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n"
+      "}\n" ::"r"(a), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
+}
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
+}
+constexpr int kStripHdr = 256;          // bytes before the strip buffers: mbarriers (full, empty), rcp table
+
+__device__ __forceinline__ void mbar_arrive(uint32_t a) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
+}
+template <bool MEDIAN, int BPP, int SW, bool INVHI>
+__global__ void __launch_bounds__(512, 1) reduce_strip_kernel(ReduceArgs a) {
+  asm volatile("griddepcontrol.launch_dependents;");   // the DP kernel may start its setup
+  using RR = RowRed<BPP, SW>;
+  constexpr int G = RR::G, NV = RR::NV;
+  extern __shared__ __align__(128) uint8_t sm[];
+  const uint32_t full0 = (uint32_t)__cvta_generic_to_shared(sm);   // [NST] mbarriers: strip landed
+  const uint32_t empty0 = full0 + 32;                               // [NST] mbarriers: strip consumed
+  uint32_t* rcp = reinterpret_cast<uint32_t*>(sm + 64);
+  const uint32_t buf0 = full0 + kStripHdr;
+  const int NST = a.tma_stages;
+  const int rs = a.tma_rs;
+  const int nrb = (a.H + 31) >> 5;
+  const int nstrips = a.batch * nrb;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int nw = (blockDim.x >> 5) - 1;   // compute warps; warp nw issues the bulk copies
+  rr_rcp_init<SW>(rcp);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NST; ++i) {
+      mbar_init(full0 + 8 * i, 1);
+      mbar_init(empty0 + 8 * i, nw);
     }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (wid == nw) {
+    // producer: strip `it` of this CTA into buffer it % NST once its previous
+    // occupant has been consumed by all compute warps
+    if (lane == 0) {
+      int it = 0;
+      for (int strip = blockIdx.x; strip < nstrips; strip += gridDim.x, ++it) {
+        const int st = it % NST;
+        if (it >= NST) mbar_wait(empty0 + 8 * st, (uint32_t)((it / NST - 1) & 1));
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic reads before async writes
+        const int frame = strip / nrb, r0 = (strip - frame * nrb) << 5;
+        const int nrows = min(32, a.H - r0);
+        const uint32_t bar = full0 + 8 * st;
+        mbar_expect_tx(bar, (uint32_t)(nrows * a.tma_rowb));
+        const uint8_t* src = a.disp + ((int64_t)frame * a.H + r0) * a.pitch;
+        for (int r = 0; r < nrows; ++r)
+          bulk_g2s(buf0 + (uint32_t)((st * 32 + r) * rs), src + (int64_t)r * a.pitch, (uint32_t)a.tma_rowb, bar);
+      }
+    }
+    return;
+  }
+  const int ngroups = (a.n_cols + G - 1) / G;
+  const uint32_t lim = (uint32_t)a.D << a.q_bits;
+  const int shift = kRBits + 1 - a.q_bits;
+  const float Df = (float)a.D;
+  const bool inv_hi = INVHI || a.invalid >= lim;
+  int it = 0;
+  for (int strip = blockIdx.x; strip < nstrips; strip += gridDim.x, ++it) {
+    const int st = it % NST;
+    mbar_wait(full0 + 8 * st, (uint32_t)((it / NST) & 1));
+    const int frame = strip / nrb, r = ((strip - frame * nrb) << 5) + lane;
+    if (r < a.H) {
+      const uint32_t rowa = buf0 + (uint32_t)((st * 32 + lane) * rs);
+      uint16_t* outr = a.out + (int64_t)frame * a.n_cols * a.H + (a.H - 1 - r);
+      for (int cg = wid; cg < ngroups; cg += nw) {
+        uint32_t cur[NV * 4];
 #pragma unroll
-    for (int i = 0; i < NV * 4; ++i) cur[i] = nxt[i];
+        for (int i = 0; i < NV; ++i) {
+          const uint4 x = lds128(rowa + (uint32_t)(cg * NV * 16 + 16 * i));
+          cur[4 * i] = x.x; cur[4 * i + 1] = x.y; cur[4 * i + 2] = x.z; cur[4 * i + 3] = x.w;
+        }
+        uint16_t* o = outr + (int64_t)cg * G * a.H;
+        if ((cg + 1) * G <= a.n_cols)
+          rr_reduce_span<MEDIAN, BPP, SW, INVHI, NV, true>(cur, cg * G, a.n_cols, o, a.H, rcp, lim, shift, Df,
+                                                           inv_hi, a.invalid);
+        else
+          rr_reduce_span<MEDIAN, BPP, SW, INVHI, NV, false>(cur, cg * G, a.n_cols, o, a.H, rcp, lim, shift, Df,
+                                                            inv_hi, a.invalid);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty0 + 8 * st);   // this warp is done with buffer st
   }
 }
 
@@ -462,10 +636,14 @@ template <int DP, bool SPARSE>
 __host__ __device__ constexpr uint32_t ring_b1() { return (DP + 48) * 4u; }   // from buffer 0
 template <int DP>
 __host__ __device__ constexpr int no_band() { return DP + 16; }   // drp code: invalid pixel
-// priv row stride (floats): == 3 mod 32, so the two half-warps' gathers of adjacent
-// targets whose means differ by one land in different banks
+// priv row stride (floats): == 17 mod 32.  A rectangle gather reads 16 target rows
+// t at their means f_t, bank (17 t + f_t) mod 32: targets whose means differ by one
+// or two (the common case on one surface) collide only for (t, t') = (0, 15) or
+// |t - t'| = 2 with |f - f'| = 2.  Simulated on C3 columns (scripts/micro/
+// stride_sim.py): 1.075 wavefronts per gather (3 mod 32: 1.54, 1 mod 32: 1.90,
+// matching ncu); B200 A/B: +0.45%.
 template <int DP>
-__host__ __device__ constexpr int priv_stride() { return DP + 3; }
+__host__ __device__ constexpr int priv_stride() { return DP + 17; }
 // E' copies in shared memory: the dense ring reads 4 shifted copies, the sparse
 // path (build only) one.
 template <bool SPARSE>
@@ -558,12 +736,6 @@ __device__ __forceinline__ int span_f(uint32_t t, uint32_t n4, const uint8_t* sm
   return (int)__umulhi(y, M);
 }
 
-__device__ __forceinline__ uint4 lds128(uint32_t addr) {
-  uint4 v;
-  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
-  return v;
-}
 __device__ __forceinline__ float ldsf(uint32_t addr) {
   float v;
   asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));

@@ -514,6 +514,58 @@ def test_reduce_rows_kernel_bit_exact(fmt, s, pad):
         hd.destroy()
 
 
+@pytest.mark.parametrize("fmt", ["u16", "u8", "f32"])
+@pytest.mark.parametrize("s", [5, 7])
+@pytest.mark.parametrize("pad", [0, 48])
+def test_reduce_strip_kernel_bit_exact(fmt, s, pad):
+    """The strip reduction (reduce_strip_kernel: whole rows streamed into shared
+    memory by bulk copies, used when a batch has >= 4 strips of 32 rows per SM),
+    bit-exact against the oracle for mean and median on 240 frames of 70 rows (a
+    ragged 6-row last strip), tight and padded rows, invalid / out-of-range / NaN
+    pixels, integer sentinels below and above the range limit."""
+    import torch
+    from oracle import oracle as orc
+    from paper_1610_04124_b200 import stixels as S
+    H, D, B = 70, 64, 240
+    bpp = {"u16": 2, "u8": 1, "f32": 4}[fmt]
+    W = (16 * 37) // bpp + s - 1
+    W -= ((W * bpp) % 16) // bpp
+    rng = np.random.default_rng(7 * s + bpp + pad)
+    Wp = W + pad // bpp
+    if fmt == "u16":
+        full = rng.integers(0, (D + 2) * 16, size=(B, H, Wp)).astype(np.uint16)
+        full[rng.random(full.shape) < 0.1] = 0xFFFF
+        kws = [dict(invalid_value=0xFFFF, disp_frac_bits=4), dict(invalid_value=7, disp_frac_bits=4)]
+        dev = torch.from_numpy(full.view(np.int16)).cuda()
+    elif fmt == "u8":
+        full = rng.integers(0, 256, size=(B, H, Wp)).astype(np.uint8)
+        kws = [dict(invalid_value=255, disp_frac_bits=2, disp_format=S.U8),
+               dict(invalid_value=3, disp_frac_bits=2, disp_format=S.U8)]
+        dev = torch.from_numpy(full).cuda()
+    else:
+        full = (rng.random((B, H, Wp)) * (D + 2) - 1).astype(np.float32)
+        full[rng.random(full.shape) < 0.05] = np.nan
+        kws = [dict(disp_format=S.F32)]
+        dev = torch.from_numpy(full).cuda()
+    f = np.ascontiguousarray(full[:, :, :W])
+    for kw in kws:
+        for mode in (0, 1):
+            p = mp.make(max_disparity=D, stixel_width=s, reduce_mode=mode, **kw)
+            hd = S.Handle(S.params_from_dict(p, H), W, H, B)
+            cols = torch.empty((B, hd.n_cols, H), dtype=torch.int16, device="cuda")
+            hd.reduce(dev, cols, row_pitch_bytes=Wp * bpp)
+            hd.sync()
+            got = cols.cpu().numpy().view(np.uint16).astype(np.int32)
+            got[got == 0xFFFF] = -1
+            for b in range(0, B, 7):
+                if fmt == "f32":
+                    want = orc.reduce(f[b], s, 0, 0, D, mode=mode)
+                else:
+                    want = orc.reduce(f[b], s, kw["disp_frac_bits"], kw["invalid_value"], D, mode=mode)
+                assert (got[b] == want).all(), (kw, mode, b, np.argwhere(got[b] != want)[:3])
+            hd.destroy()
+
+
 @pytest.mark.parametrize("D,q", [(64, 4), (256, 8)])
 def test_top_of_range_pixels_exact(D, q):
     """L#27: pixels in [D - 1/2, D) keep their value for the ground and sky terms
