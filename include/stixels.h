@@ -234,6 +234,18 @@ int stixels_last_launch_count(const stixels_handle* h);
  * Errors: ARG (h NULL). */
 int stixels_query_launch(const stixels_handle* h, int* warps_per_column, int* cols_per_cta);
 
+/* Exact chunk bound of the int32 (STIXELS_DP_INT32) DP kernel: the cumulative
+ * number of DP cells (bottom x target pairs of 32 x 32 rectangle chunks) that
+ * the kernel skipped since the handle was created, because a lower bound on
+ * every candidate of the chunk (each pixel costs at least Pair(0); pixels of the
+ * rows between the chunk and the target block that no one mean's band can hold
+ * cost the outlier cap, Eq. 4 / P:113) exceeded the best candidate already found
+ * for every target of the block.  Skipped candidates are strictly worse than the
+ * minimum, so costs and stixel lists are unchanged; the count lets a benchmark
+ * separate evaluated from algorithmic cells.  Synchronises the handle's streams.
+ * Errors: ARG (h or cells NULL), CUDA. */
+int stixels_skipped_cells(stixels_handle* h, unsigned long long* cells);
+
 /* Launch plan of the DP kernel for the following calls: 0 = automatic (the
  * default: 8 warps per column when a batch has at most 2 columns per SM, else
  * 4), 4 or 8 = forced (tests cover both plans on every shape; 8 on a full batch

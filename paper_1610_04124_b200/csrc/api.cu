@@ -43,6 +43,7 @@ struct stixels_handle {
   int* d_dgR = nullptr;
   uint32_t* d_thr = nullptr;
   int* d_overflow = nullptr;
+  unsigned long long* d_skipped = nullptr;   // IW chunk bound: cumulative skipped cells
   float* d_scratch = nullptr;   // per-column-slot DP scratch of h->stream (and hs[0])
   uint16_t* d_cols = nullptr;   // reduced columns of the two-launch plan [max_batch][n_cols][H]
   size_t scratch_bytes = 0;
@@ -263,7 +264,7 @@ const char* stixels_last_error(const stixels_handle* h) {
 
 static void free_all(stixels_handle* h) {
   cudaFree(h->d_E); cudaFree(h->d_E2); cudaFree(h->d_WT); cudaFree(h->d_M2); cudaFree(h->d_gG); cudaFree(h->d_gS);
-  cudaFree(h->d_dgR); cudaFree(h->d_thr); cudaFree(h->d_overflow); cudaFree(h->d_scratch); cudaFree(h->d_cols);
+  cudaFree(h->d_dgR); cudaFree(h->d_thr); cudaFree(h->d_overflow); cudaFree(h->d_skipped); cudaFree(h->d_scratch); cudaFree(h->d_cols);
   cudaFree(h->hscratch1);
   if (h->ev_entry) cudaEventDestroy(h->ev_entry);
   for (int i = 0; i < 2; ++i) {
@@ -528,6 +529,7 @@ int stixels_create(const stixels_params* params, int width, int height, int max_
       (e = alloc((void**)&h->d_dgR, dgR.size() * 4)) != cudaSuccess ||
       (e = alloc((void**)&h->d_thr, thrg.size() * 4)) != cudaSuccess ||
       (e = alloc((void**)&h->d_overflow, 4)) != cudaSuccess ||
+      (e = alloc((void**)&h->d_skipped, 8)) != cudaSuccess ||
       (e = alloc((void**)&h->d_scratch, h->scratch_bytes = (size_t)h->grid * cpc * 4 *
                         (DPv == 128 ? col_scratch_floats<128>(height) : col_scratch_floats<256>(height)))) != cudaSuccess ||
       (e = alloc((void**)&h->d_cols, (size_t)max_batch * h->n_cols * height * 2)) != cudaSuccess)
@@ -539,10 +541,21 @@ int stixels_create(const stixels_params* params, int width, int height, int max_
   cudaMemcpy(h->d_dgR, dgR.data(), dgR.size() * 4, cudaMemcpyHostToDevice);
   cudaMemcpy(h->d_thr, thrg.data(), thrg.size() * 4, cudaMemcpyHostToDevice);
   cudaMemset(h->d_overflow, 0, 4);
+  cudaMemset(h->d_skipped, 0, 8);
   e = cudaDeviceSynchronize();
   if (e != cudaSuccess) return bail(STIXELS_ERR_CUDA, std::string("table upload: ") + cudaGetErrorString(e));
   A.E = h->d_E; A.E2g = h->d_E2; A.WTg = h->d_WT; A.M2 = h->d_M2; A.gG = h->d_gG; A.gS = h->d_gS; A.dgR = h->d_dgR; A.thrg = h->d_thr;
   A.overflow = h->d_overflow;
+  A.skipped = h->d_skipped;
+  // exact chunk bound of the int32 kernel: on for columns of >= kBoundMinH rows
+  // (B200 f1 sweep: +5% at h = 440, +15% at 880, +25% at 1024; -6% at 220, where
+  // its per-column tables cost more than the few far chunks it skips) whose P2
+  // table fits the eo words' free low halves (nb * DP / 8 <= h + 2)
+  {
+    constexpr int kBoundMinH = 320;
+    const int nbk = (height + 31) / 32;
+    A.bound = (iw && height >= kBoundMinH && nbk * (DPv / 8) <= height + 2) ? 1 : 0;
+  }
   A.scratch = h->d_scratch;
   *out = h;
   return STIXELS_OK;
@@ -842,6 +855,16 @@ int stixels_set_launch_plan(stixels_handle* h, int warps_per_column) {
   if (warps_per_column == 8 && h->cols_per_cta8 < 1)
     return fail(h, STIXELS_ERR_UNSUPPORTED, "8 warps per column: shared memory too small for this shape");
   h->plan_cw = warps_per_column;
+  return STIXELS_OK;
+}
+
+int stixels_skipped_cells(stixels_handle* h, unsigned long long* cells) {
+  if (!h || !cells) return STIXELS_ERR_ARG;
+  cudaSetDevice(h->device);
+  CU(cudaStreamSynchronize(h->stream), h);
+  if (h->hs[0]) CU(cudaStreamSynchronize(h->hs[0]), h);
+  if (h->hs[1]) CU(cudaStreamSynchronize(h->hs[1]), h);
+  CU(cudaMemcpy(cells, h->d_skipped, 8, cudaMemcpyDeviceToHost), h);
   return STIXELS_OK;
 }
 

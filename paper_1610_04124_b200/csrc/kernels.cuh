@@ -589,6 +589,8 @@ struct DPArgs {
                            // for pixel disparity d = 0..D, row D+1 = 0 (invalid pixel)
   const float* WTg;        // NEXT f2: [DP+17][16] band weights cap - Pair[d+o-7][d] at row d+1
   int gG_stride;
+  unsigned long long* skipped;   // IW: cumulative rectangle cells skipped by the chunk bound (or null)
+  int bound;                     // IW: chunk bound on (host: columns of >= kBoundMinH rows)
 #ifdef STX_TRACE
   unsigned long long* trace;     // diagnostic build only: [4 groups][64 blocks][32] globaltimer stamps
 #endif
@@ -615,6 +617,13 @@ struct ColSmem {
   float2* part;     // [4][32]        partial minima {cost, argj} of the 4 warps
   float4* pgps;     // [32]           serial warp: {PG[k], PG[k+1], PS[k], PS[k+1]}
   int* ctr;         // [1]            dynamic chunk counter
+  int* ub;          // [32]           IW: per-target best candidate so far of the block's bulk chunks
+                    //                (shifted, unscaled quanta), the chunk bound's upper side
+  int* gmin;        // [nb+1]         IW: G[m] = min over chunk m's bottoms j of (least prior term of
+                    //                record j + wtmax j), the chunk bound's lower side
+                    // (and, IW only, the lo16 halves of eo -- the dense ring's window offsets,
+                    // unused by the sparse kernels -- hold P2[b][c], b >= 1: the valid pixels
+                    // of rows < 32 b whose object disparity falls in bins c or c+1 of 8)
 };
 
 constexpr int kTri = 496;              // cells of a 32-row triangle: sum_{j'<31} (31 - j')
@@ -668,9 +677,15 @@ __host__ __device__ inline int col_smem_bytes(int h) {
   b += al16(h);
   b += al16(CW * 32 * 8);
   b += al16(32 * 16);
-  b += 16;
+  b += 16;          // ctr
+  b += 32 * 4;      // ub
+  b += al16((((h + 31) >> 5) + 1) * 4);   // gmin
   return b;
 }
+// IW chunk bound: disparity bins of 8 (pixel-count prefixes per bin pair at block
+// boundaries)
+template <int DP>
+__host__ __device__ constexpr int bound_bins() { return DP / 8; }
 // global scratch per column slot: PG[h+1], PS[h+1], anchor rows [nb+1][DP]
 template <int DP>
 __host__ __device__ inline int64_t col_scratch_floats(int h) {
@@ -692,7 +707,9 @@ __device__ inline ColSmem carve(uint8_t* p, int h) {
   w.fpv = p; p += al16(h);
   w.part = reinterpret_cast<float2*>(p); p += al16(CW * 32 * 8);
   w.pgps = reinterpret_cast<float4*>(p); p += al16(32 * 16);
-  w.ctr = reinterpret_cast<int*>(p);
+  w.ctr = reinterpret_cast<int*>(p); p += 16;
+  w.ub = reinterpret_cast<int*>(p); p += 32 * 4;
+  w.gmin = reinterpret_cast<int*>(p);
   return w;
 }
 
@@ -850,8 +867,10 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
   uint32_t* M2s = reinterpret_cast<uint32_t*>(smem + kM2Pad);
   float* E = reinterpret_cast<float*>(smem + kM2Pad + al16((h + 1) * 4));
   uint16_t* tri_jk = reinterpret_cast<uint16_t*>(smem + kM2Pad + al16((h + 1) * 4) + e_copies<SPARSE>() * a.esz * 4);
+#pragma unroll 1
   for (int i = threadIdx.x; i <= h; i += blockDim.x) M2s[i] = a.M2[i];
   // IW: the object pair-cost window in int32 quanta (exact-mode costs are integers)
+#pragma unroll 1
   for (int i = threadIdx.x; i < e_copies<SPARSE>() * a.esz; i += blockDim.x) {
     if constexpr (IW) reinterpret_cast<int*>(E)[i] = __float2int_rn(a.E[i]) * kIWS;
     else E[i] = a.E[i];
@@ -861,8 +880,10 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
     for (int i = threadIdx.x; i < wt_rows<DP>() * 16; i += blockDim.x) WT[i] = a.WTg[i];
   // gravity thresholds {thrA1[j], thrB[j]} per row (one LDS.64 per row in the rectangle)
   int2* thrS = reinterpret_cast<int2*>(reinterpret_cast<uint8_t*>(WT) + (PAIR2D && SPARSE ? wt_rows<DP>() * 16 * 4 : 0));
+#pragma unroll 1
   for (int i = threadIdx.x; i < h; i += blockDim.x) thrS[i] = make_int2(a.thrA1[i], a.thrB[i]);
   const uint32_t thr_s = (uint32_t)__cvta_generic_to_shared(thrS);
+#pragma unroll 1
   for (int jp = 0; jp < 31; ++jp)                 // triangle cell index -> (j', k')
     for (int kp = jp + 1 + (int)threadIdx.x; kp < 32; kp += blockDim.x)
       tri_jk[tri_off(jp) + kp - jp - 1] = (uint16_t)(jp | (kp << 8));
@@ -883,6 +904,17 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
   float* PGg = a.scratch + (int64_t)slot_global * col_scratch_floats<DP>(h);
   float* PSg = PGg + (h + 1);
   float* ANg = PSg + (h + 1);          // anchor W-rows W[.][32m], global (L2)
+  // IW chunk bound (L2): P2[b][c] = valid pixels of rows < 32 b whose object
+  // disparity falls in bins c or c+1 (of 8), G[m] = min over chunk m's bottoms j
+  // of (min prior term of record j + wtmax j)
+  constexpr int NBIN = bound_bins<DP>();
+  // P2[b][c] (b >= 1) in the lo16 half of eo word (b - 1) NBIN + c; P2[0][.] = 0
+  uint16_t* P2s = reinterpret_cast<uint16_t*>(cs.eo);
+  auto p2_at = [&](int b, int c) { return b > 0 ? (int)P2s[2 * ((b - 1) * NBIN + c)] : 0; };
+  const bool bound = IW && a.bound;    // host: tall enough columns
+  const int wtmax = IW ? (int)a.wt[7] : 0;   // cap - Pair(0): the largest band weight (quanta)
+  constexpr int kUBInf = 0x3fffffff;
+  unsigned long long skipped = 0;      // cells of chunks skipped by this warp
 
   // sparse update lanes: lanes 0-14 serve W-row buffer 1 (odd bottoms), lanes
   // 16-30 buffer 0 (even bottoms); each owns one offset d = (lane & 15) - 7 of
@@ -1066,12 +1098,14 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
       }
     }
     if constexpr (IW) {
-      // a run lies inside one 32-row block: bottom = block base + low bits; runs
-      // come in increasing j per warp, so an equal cost keeps the earlier bottom
+      // a run lies inside one 32-row block: bottom = block base + low bits; bulk
+      // chunks come nearest first (decreasing j), so an equal cost takes the lower
+      // bottom (L#17)
       const int jb = ((j0 - 1) & ~31) + 1;
       auto fold = [&](int m, CT& best, int& argj) {
         const int c = m >> 5;            // arithmetic: floor((cost x 32 + off) / 32) = cost
-        if (m != 0x7fffffff && c < best) { best = c; argj = jb + (m & 31); }
+        const int jm = jb + (m & 31);
+        if (m != 0x7fffffff && (c < best || (c == best && jm < argj))) { best = c; argj = jm; }
       };
       fold(m0, acc.b0, acc.a0);
       fold(m1, acc.b1, acc.a1);
@@ -1091,23 +1125,61 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
     return make_float2(mf, __int_as_float(ma));
   };
 
-  // Full 32-row chunks m < mend for this warp's targets, handed out dynamically;
-  // the anchor row of the next chunk is prefetched from L2 while one runs.
-  auto bulk_chunks = [&](int mend, const Tg& tg, Acc& acc) {
+  // Full 32-row chunks m < mend for this warp's targets, handed out dynamically
+  // (IW: nearest first, m = mend - 1 down to 0, so the chunk bound meets a tight
+  // best candidate; the fp32 paths keep increasing m, which their strict-less
+  // running minima need for L#17's first-bottom ties); the anchor row of the next
+  // chunk is prefetched from L2 while one runs.
+  // IW chunk bound (branch and bound, exact): every candidate of chunk m for a
+  // target k of block B = mend + 1 satisfies
+  //   cand(j, k) >= G[m] + wtmax (|S| - maxcount(S)) - wtmax (k + 1)
+  // (shifted, unscaled), S = rows [32(m+1), 32B) inside every span [j, k]: each
+  // pixel costs at least Pair(0) = cap - wtmax, and every pixel of S outside the
+  // band of the span's mean costs cap (Eq. 4 saturates); maxcount(S) <=
+  // max_c (P2[B][c] - P2[m+1][c]) bounds the pixels any one mean's band can hold.
+  // The chunk is skipped when that bound exceeds, for every target, the best
+  // candidate found so far by any warp (ub, strictly: a skipped candidate can be
+  // neither the minimum nor tied with it, so costs and argmins are unchanged).
+  auto bulk_chunks = [&](int mend, const Tg& tg, Acc& acc, int Kn) {
     int m = 0;
     if (lane == 0) m = atomicAdd(cs.ctr, 1);
     m = __shfl_sync(0xffffffffu, m, 0);
+    auto chunk_of = [&](int q) { return IW ? mend - 1 - q : q; };
     float rr[4 * NR];
-    if (m < mend) load_seed(rr, ANg + m * DP);
+    if (m < mend) load_seed(rr, ANg + chunk_of(m) * DP);
+    // bound inputs of block B = mend + 1 (this lane: bin c = lane)
+    const int p2B = (bound && lane < NBIN) ? p2_at(mend + 1, lane) : 0;
+    const int kl = min(Kn + lane, h - 1);
     while (m < mend) {
+      const int mc = chunk_of(m);      // this chunk
       int m2 = 0;
       if (lane == 0) m2 = atomicAdd(cs.ctr, 1);
       m2 = __shfl_sync(0xffffffffu, m2, 0);
       float nx[4 * NR];
 #pragma unroll
       for (int i = 0; i < 4 * NR; ++i) nx[i] = 0.f;
-      if (m2 < mend) load_seed(nx, ANg + m2 * DP);
-      rect_run(rr, 32 * m + 1, 32, tg, acc);
+      if (m2 < mend) load_seed(nx, ANg + chunk_of(m2) * DP);
+      bool skip = false;
+      if (bound) {
+        const int X = __reduce_max_sync(0xffffffffu, cs.ub[lane] + wtmax * (kl + 1));
+        if (X < kUBInf) {                // (warp-uniform) some candidate of every target is known
+          const int p2n = lane < NBIN ? p2_at(mc + 1, lane) : 0;
+          const int maxcount = __reduce_max_sync(0xffffffffu, p2B - p2n);
+          skip = cs.gmin[mc] + wtmax * (32 * (mend - mc) - maxcount) > X;
+        }
+      }
+      if (!skip) {
+        rect_run(rr, 32 * mc + 1, 32, tg, acc);
+        if constexpr (IW) {
+          if (bound) {
+            // publish this warp's per-target minima (both halves merged): lane l -> target l
+            const int o0 = __shfl_xor_sync(0xffffffffu, acc.b0, 16), o1 = __shfl_xor_sync(0xffffffffu, acc.b1, 16);
+            atomicMin(cs.ub + lane, hw ? min(acc.b1, o1) : min(acc.b0, o0));
+          }
+        }
+      } else {
+        skipped += 32ull * (unsigned)min(32, h - Kn);
+      }
 #pragma unroll
       for (int i = 0; i < 4 * NR; ++i) rr[i] = nx[i];
       m = m2;
@@ -1152,6 +1224,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
       __syncwarp();
       stixel_t* o = a.out + (int64_t)item * a.cap;
       const int nw = min(n, a.cap);
+#pragma unroll 1
       for (int i = lane; i < nw; i += 32) {
         uint2 e = lst[n - 1 - i];
         stixel_t s;
@@ -1265,14 +1338,18 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
         const float* src = (w == 0) ? tG : tS;
         float* dst = (w == 0) ? PGg : PSg;
         float tot = 0.f;
+#pragma unroll 1
         for (int v = s0; v < s1; ++v) tot += src[v];
         float acc = warp_incl_scan(tot, lane) - tot;   // exclusive prefix of the totals
         if (lane == 0) dst[0] = 0.f;
+#pragma unroll 1
         for (int v = s0; v < s1; ++v) { acc += src[v]; dst[v + 1] = acc; }
       } else {
         uint32_t tot = 0;
+#pragma unroll 1
         for (int v = s0; v < s1; ++v) { const uint32_t t = tD[v]; tot += (w == 2) ? t : (t ? 4u : 0u); }
         uint32_t acc = warp_incl_scan(tot, lane) - tot;
+#pragma unroll 1
         for (int v = s0; v < s1; ++v) {
           const uint32_t t = tD[v];
           acc += (w == 2) ? t : (t ? 4u : 0u);
@@ -1297,7 +1374,9 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
       const uint32_t eor = cs.eo[K0b + min(lane, rows - 1)] >> 16;
       const uint32_t dst_s = (uint32_t)__cvta_generic_to_shared(cs.priv) + lane * 4;
       const uint32_t src_s = (uint32_t)__cvta_generic_to_shared(E) + lane * 4;
-#pragma unroll
+      // (not unrolled: four copies of this batch of 8 rows, whose shuffles the
+      // compiler wraps in collective sequences, cost instruction-cache misses)
+#pragma unroll 1
       for (int i0 = 0; i0 < 32; i0 += 8) {
         if (i0 < rows) {
           CT x[8][NB];
@@ -1395,6 +1474,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
         for (int i = 1; i < NWN; ++i) {
           float* sd = cs.seed + ((bt & 1) * (NWN - 1) + i - 1) * DP;
           const float* row = cs.priv + (32 / NWN * i - 1) * priv_stride<DP>();
+#pragma unroll 1
           for (int f = lane; f < DP; f += 32) sd[f] = row[f];
         }
       }
@@ -1404,7 +1484,30 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
 #pragma unroll
       for (int c = 0; c < NB; ++c) fr[c] = 0;
       build_priv(0);
+    } else if (bound && w == 3) {
+      // chunk-bound tables while warps 1-2 build: P2 at every block boundary (bins
+      // of 8 of the pixels' object disparities).  Per block, the lanes (rows) that
+      // share a bin find each other with one match; the group's first lane writes
+      // the count into a per-bin scratch row (cs.part, free until block 0's merge)
+      int* hb = reinterpret_cast<int*>(cs.part);
+      int pc = 0;                        // lane c: valid pixels of bin c in rows < 32 bb
+#pragma unroll 1
+      for (int bb = 0; bb < nb; ++bb) {
+        const int v = (bb << 5) + lane;
+        const uint32_t code = v < h ? cs.rec[2 * v + 1].w >> 16 : (uint32_t)kNoBand;
+        const int bin = code != (uint32_t)kNoBand ? (int)(code - 1) >> 3 : 255;   // round(d) >> 3
+        hb[lane] = 0;
+        __syncwarp();
+        const uint32_t same = __match_any_sync(0xffffffffu, bin);
+        if (bin < NBIN && (same & ((1u << lane) - 1)) == 0) hb[bin] = __popc(same);
+        __syncwarp();
+        pc += hb[lane];
+        __syncwarp();
+        const int up = __shfl_down_sync(0xffffffffu, pc, 1);
+        if (lane < NBIN) P2s[2 * (bb * NBIN + lane)] = (uint16_t)(pc + (lane + 1 < NBIN ? up : 0));
+      }
     }
+    if (bound && ctid < 32) cs.ub[ctid] = kUBInf;
     named_bar(bar_col, CW * 32);
     if (w == 0) STX_STAMP(60, 5);       // block 0's priv rows built
 
@@ -1617,6 +1720,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
         // every lane now holds the final values of its target row k: write the
         // record of row k+1 (consumed by later rectangles; predecessor terms
         // shifted by -cap*(k+1)) and the index table
+        int gv = 0x7fffffff;
         if (k < h) {
           const float sh = capQ * (float)(k + 1);
           // IW: int32 quanta x 32 with (j - 1) & 31 = k & 31 of row j = k + 1 in the low bits
@@ -1653,6 +1757,12 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
           cs.argG[k] = (uint16_t)aG;
           cs.argS[k] = (uint16_t)aS;
           cs.fpv[k] = (uint8_t)argf;
+          if constexpr (IW)                // chunk bound: min prior term of bottom j = k + 1, + wtmax j
+            gv = (min(min((int)V0, (int)V1), min((int)V2, (int)V3)) >> 5) + wtmax * (k + 1);
+        }
+        if (bound) {
+          const int g = __reduce_min_sync(0xffffffffu, gv);   // chunk b = bottoms 32b+1 .. 32b+32
+          if (lane == 0) cs.gmin[b] = g;
         }
         STX_STAMP(b, 1);
         if (has_next) named_bar(bar_x, CW * 32);   // block b+1's priv rows are ready
@@ -1690,7 +1800,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
           if (w == NWN) copy_seed(bn);
         }
         // full chunks m <= b-1: their records (rows <= 32 b) were final before block b
-        bulk_chunks(b, tg, acc);
+        bulk_chunks(b, tg, acc, Kn);
       }
       // warp 0's newest-chunk seed W[.][K0] from L2, prefetched before the barrier
       float rs0[4 * NR];
@@ -1718,6 +1828,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
         }
         cs.part[w * 32 + lane] = merge_part(acc);
         if (ctid == 0) *cs.ctr = 0;
+        if (bound && ctid < 32) cs.ub[ctid] = kUBInf;   // (read again only after the next bar_col)
       }
       STX_STAMP(b, 12 + w);
       named_bar(bar_col, CW * 32);
@@ -1730,6 +1841,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
     if (w == 0) { pend_item = item; pendO = lastO; pendG = lastG; pendS = lastS; }
   }
   if (w == 0 && pend_item >= 0) backtrack(pend_item, pendO, pendG, pendS);
+  if (bound && a.skipped && lane == 0 && skipped) atomicAdd(a.skipped, skipped);
 }
 
 }  // namespace stx

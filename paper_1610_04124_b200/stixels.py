@@ -90,6 +90,8 @@ def lib() -> ctypes.CDLL:
         L.stixels_last_launch_count.argtypes = [vp]
         L.stixels_query_launch.argtypes = [vp, P(i32), P(i32)]
         L.stixels_set_launch_plan.argtypes = [vp, i32]
+        if hasattr(L, "stixels_skipped_cells"):   # (absent from A/B builds that predate it)
+            L.stixels_skipped_cells.argtypes = [vp, P(ctypes.c_ulonglong)]
         L.stixels_destroy.argtypes = [vp]
         L.stixels_error_string.argtypes = [i32]
         L.stixels_error_string.restype = ctypes.c_char_p
@@ -107,7 +109,7 @@ EXPORTS = ("stixels_default_params", "stixels_create", "stixels_query", "stixels
            "stixels_compute",
            "stixels_compute_host", "stixels_reduce", "stixels_solve", "stixels_sync",
            "stixels_last_launch_count", "stixels_query_launch", "stixels_set_launch_plan",
-           "stixels_destroy", "stixels_error_string",
+           "stixels_skipped_cells", "stixels_destroy", "stixels_error_string",
            "stixels_last_error")
 
 
@@ -234,6 +236,12 @@ class Handle:
     def set_launch_plan(self, warps_per_column: int) -> None:
         """0 = automatic, 4 or 8 warps per column (stixels_set_launch_plan)."""
         _check(lib().stixels_set_launch_plan(self._h, warps_per_column), self._h)
+
+    def skipped_cells(self) -> int:
+        """Cumulative DP cells skipped by the exact chunk bound (stixels_skipped_cells)."""
+        n = ctypes.c_ulonglong()
+        _check(lib().stixels_skipped_cells(self._h, ctypes.byref(n)), self._h)
+        return n.value
 
     def last_launch_shape(self) -> tuple[int, int]:
         """(warps per column, column groups per CTA) of the last DP launch."""
