@@ -611,20 +611,25 @@ def main():
     peak_tops = n_sm * 4 * 32 * sm_max * 1e6 / 1e12       # lane-instruction issue peak
     dp_ms = statistics.mean(dp)
     cells = cells_per_frame() * B
-    # the exact chunk bound skips rectangle cells whose candidates are provably worse
-    # than a known one (stixels_skipped_cells): `achieved` counts the cells the kernel
-    # evaluated, so `frac` stays a measure of how the hardware is used
+    # `achieved` counts the algorithmic cells of the launch (every (column, target,
+    # bottom) of Eq. 6).  The int32 kernel's exact chunk bound skips rectangle cells
+    # whose candidates are provably worse than a known one (stixels_skipped_cells);
+    # `evaluated` reports the same rate over the cells the kernel actually computed,
+    # which is the measure of how the hardware is used
     evaluated = cells - skipped_per_launch
-    achieved = evaluated * ALG_OPS_PER_CELL / (dp_ms / 1000.0) / 1e12
+    achieved = cells * ALG_OPS_PER_CELL / (dp_ms / 1000.0) / 1e12
+    ach_eval = evaluated * ALG_OPS_PER_CELL / (dp_ms / 1000.0) / 1e12
     prof = ncu_profile()
     tpf = prof.get("dram_bytes_per_frame")
     roofline = {"bound": "alu", "achieved": achieved, "peak": peak_tops, "unit": "Tops/s",
                 "frac": achieved / peak_tops,
                 "traffic": (tpf * B) if tpf is not None else None,
                 "kernel": "dp_kernel", "ops_per_cell": ALG_OPS_PER_CELL,
-                "cells_per_launch": cells, "cells_evaluated_per_launch": evaluated,
-                "cells_skipped_frac": skipped_per_launch / cells,
-                "achieved_all_cells": cells * ALG_OPS_PER_CELL / (dp_ms / 1000.0) / 1e12,
+                "cells_per_launch": cells,
+                "evaluated": {"cells_per_launch": evaluated, "skipped_frac": skipped_per_launch / cells,
+                              "achieved": ach_eval, "frac": ach_eval / peak_tops,
+                              "note": "the same rate over the cells the kernel computed (the exact "
+                                      "chunk bound skips the rest)"},
                 "peak_note": f"{n_sm} SMs x 128 lanes x {sm_max:.0f} MHz (issue peak, "
                              "B200_PROFILING/B300_MICROARCH unit counts; DESIGN.md 5b)",
                 "ncu_pipe_util": prof.get("pipe_util")}

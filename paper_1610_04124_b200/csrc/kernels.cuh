@@ -1126,8 +1126,9 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
   };
 
   // Full 32-row chunks m < mend for this warp's targets, handed out dynamically
-  // (IW: nearest first, m = mend - 1 down to 0, so the chunk bound meets a tight
-  // best candidate; the fp32 paths keep increasing m, which their strict-less
+  // (with the chunk bound on: nearest first, m = mend - 1 down to 0, so that the
+  // far chunks meet a tight best candidate, and the run fold takes the lower
+  // bottom on equal costs; otherwise increasing m, which the fp32 paths' strict-less
   // running minima need for L#17's first-bottom ties); the anchor row of the next
   // chunk is prefetched from L2 while one runs.
   // IW chunk bound (branch and bound, exact): every candidate of chunk m for a
@@ -1144,7 +1145,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
     int m = 0;
     if (lane == 0) m = atomicAdd(cs.ctr, 1);
     m = __shfl_sync(0xffffffffu, m, 0);
-    auto chunk_of = [&](int q) { return IW ? mend - 1 - q : q; };
+    auto chunk_of = [&](int q) { return bound ? mend - 1 - q : q; };
     float rr[4 * NR];
     if (m < mend) load_seed(rr, ANg + chunk_of(m) * DP);
     // bound inputs of block B = mend + 1 (this lane: bin c = lane)

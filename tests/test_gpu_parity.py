@@ -211,6 +211,27 @@ def test_c2_frames_exact():
     assert hd.last_launch_count() == 2      # reduce_kernel + dp_kernel
 
 
+def test_chunk_bound_skips_and_stays_exact():
+    """The int32 kernel's exact chunk bound (columns of >= 320 rows): on C2 frames
+    it skips a substantial share of the rectangle cells (stixels_skipped_cells) and
+    the lists and costs stay identical to the oracle's under both launch plans; on
+    two-valued striped columns (many equal-cost candidates in different chunks, so
+    the nearest-first chunk order must still resolve ties to the lower bottom, L#17)
+    and at h = 352 (a ragged last block) as well."""
+    frames = _frames_c2(2, seed0=3300)
+    p = mp.make()
+    g, gc, cnt, hd = _assert_exact(p, frames)
+    cells = hd.n_cols * 440 * 441 // 2 * frames.shape[0]
+    # (the handle of the last plan, 8 warps per column, ran once on these frames)
+    assert hd.skipped_cells() > 0.1 * cells
+    rng = np.random.default_rng(3301)
+    H, W = 352, 320
+    stripes = np.where(rng.random((2, H, 1)) < 0.5, 10 * 16, 40 * 16).astype(np.uint16)
+    fr = np.repeat(stripes, W, axis=2)
+    fr[:, rng.random(H) < 0.05, :] = 0xFFFF              # a few invalid rows
+    _assert_exact(mp.make(ground_slope=0.3), fr)
+
+
 def test_dp_variants_exact():
     """Each DP kernel variant stixels_create picks is exact against
     the oracle: the int32 atomic-band path (band <= 3, the default model), the
