@@ -637,7 +637,7 @@ def main():
     red_ms = statistics.mean(red)
     red_bytes = B * (W_IMG * H_IMG * 2 + (W_IMG // S_W) * H_IMG * 2)
     hbm_peak = peaks.get("hbm_gbs", 6555.2)
-    k1_roofline = {"bound": "hbm", "kernel": "reduce_kernel", "unit": "GB/s",
+    k1_roofline = {"bound": "hbm", "kernel": "reduce_strip_kernel", "unit": "GB/s",
                    "achieved": red_bytes / (red_ms / 1000.0) / 1e9, "peak": hbm_peak,
                    "frac": red_bytes / (red_ms / 1000.0) / 1e9 / hbm_peak,
                    "bytes_per_launch": red_bytes}
