@@ -246,6 +246,14 @@ int stixels_query_launch(const stixels_handle* h, int* warps_per_column, int* co
  * Errors: ARG (h or cells NULL), CUDA. */
 int stixels_skipped_cells(stixels_handle* h, unsigned long long* cells);
 
+/* The chunk bound for the following calls: 0 = automatic (the default: on for
+ * the int32 kernel when the height is >= 320 rows), 1 = off, 2 = on (any height
+ * whose per-block tables fit; tests compare both settings bit for bit).
+ * Errors: ARG (h NULL or another value), UNSUPPORTED (2 without the int32
+ * kernel, or when nb * DP / 8 > height + 2: the P2 table lives in the spare
+ * halves of a per-row array). */
+int stixels_set_chunk_bound(stixels_handle* h, int mode);
+
 /* Launch plan of the DP kernel for the following calls: 0 = automatic (the
  * default: 8 warps per column when a batch has at most 2 columns per SM, else
  * 4), 4 or 8 = forced (tests cover both plans on every shape; 8 on a full batch

@@ -28,6 +28,8 @@ struct stixels_handle {
   int col_bytes8 = 0, cols_per_cta8 = 0;   // CW = 8 column groups (small batches), 0 = off
   int last_cw = 0, last_cpc = 0;            // warps per column, groups per CTA of the last DP launch
   int plan_cw = 0;                          // stixels_set_launch_plan: 0 auto, 4 or 8
+  bool bound_ok = false, bound_auto = false;  // chunk bound possible / on by default
+  int bound_mode = 0;                       // stixels_set_chunk_bound: 0 auto, 1 off, 2 on
   bool sparse = true;
   bool pair2d = false;          // NEXT f2: sigma_O(f) table given
   bool iw = false;              // int32 W-rows with atomic band rounds (band <= 3, exact mode)
@@ -554,7 +556,9 @@ int stixels_create(const stixels_params* params, int width, int height, int max_
   {
     constexpr int kBoundMinH = 320;
     const int nbk = (height + 31) / 32;
-    A.bound = (iw && height >= kBoundMinH && nbk * (DPv / 8) <= height + 2) ? 1 : 0;
+    h->bound_ok = iw && nbk * (DPv / 8) <= height + 2;
+    h->bound_auto = h->bound_ok && height >= kBoundMinH;
+    A.bound = h->bound_auto ? 1 : 0;
   }
   A.scratch = h->d_scratch;
   *out = h;
@@ -689,6 +693,7 @@ static int launch_dp(stixels_handle* h, const uint16_t* d_cols, int batch, stixe
   const int cw = plan_cw(h, batch);
   const int C = std::max(1, std::min(cw == 8 ? h->cols_per_cta8 : h->cols_per_cta, need));
   A.cols_per_cta = C;
+  A.bound = h->bound_mode == 0 ? (h->bound_auto ? 1 : 0) : (h->bound_mode == 2 ? 1 : 0);
   if (cw == 8) A.col_bytes = h->col_bytes8;
   const int smem = A.shared_bytes + C * A.col_bytes;
   int grid = std::min(h->grid, (A.items + C - 1) / C);
@@ -865,6 +870,14 @@ int stixels_skipped_cells(stixels_handle* h, unsigned long long* cells) {
   if (h->hs[0]) CU(cudaStreamSynchronize(h->hs[0]), h);
   if (h->hs[1]) CU(cudaStreamSynchronize(h->hs[1]), h);
   CU(cudaMemcpy(cells, h->d_skipped, 8, cudaMemcpyDeviceToHost), h);
+  return STIXELS_OK;
+}
+
+int stixels_set_chunk_bound(stixels_handle* h, int mode) {
+  if (!h || mode < 0 || mode > 2) return STIXELS_ERR_ARG;
+  if (mode == 2 && !h->bound_ok)
+    return fail(h, STIXELS_ERR_UNSUPPORTED, "chunk bound: needs the int32 kernel and nb * DP / 8 <= height + 2");
+  h->bound_mode = mode;
   return STIXELS_OK;
 }
 

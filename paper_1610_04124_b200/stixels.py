@@ -92,6 +92,7 @@ def lib() -> ctypes.CDLL:
         L.stixels_set_launch_plan.argtypes = [vp, i32]
         if hasattr(L, "stixels_skipped_cells"):   # (absent from A/B builds that predate it)
             L.stixels_skipped_cells.argtypes = [vp, P(ctypes.c_ulonglong)]
+            L.stixels_set_chunk_bound.argtypes = [vp, i32]
         L.stixels_destroy.argtypes = [vp]
         L.stixels_error_string.argtypes = [i32]
         L.stixels_error_string.restype = ctypes.c_char_p
@@ -109,7 +110,7 @@ EXPORTS = ("stixels_default_params", "stixels_create", "stixels_query", "stixels
            "stixels_compute",
            "stixels_compute_host", "stixels_reduce", "stixels_solve", "stixels_sync",
            "stixels_last_launch_count", "stixels_query_launch", "stixels_set_launch_plan",
-           "stixels_skipped_cells", "stixels_destroy", "stixels_error_string",
+           "stixels_skipped_cells", "stixels_set_chunk_bound", "stixels_destroy", "stixels_error_string",
            "stixels_last_error")
 
 
@@ -242,6 +243,10 @@ class Handle:
         n = ctypes.c_ulonglong()
         _check(lib().stixels_skipped_cells(self._h, ctypes.byref(n)), self._h)
         return n.value
+
+    def set_chunk_bound(self, mode: int) -> None:
+        """0 = automatic, 1 = off, 2 = on (stixels_set_chunk_bound)."""
+        _check(lib().stixels_set_chunk_bound(self._h, mode), self._h)
 
     def last_launch_shape(self) -> tuple[int, int]:
         """(warps per column, column groups per CTA) of the last DP launch."""

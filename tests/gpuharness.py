@@ -8,10 +8,11 @@ from tests import modelparams as mp
 
 
 def run_gpu(p: dict, frames: np.ndarray, max_batch: int | None = None, host: bool = False,
-            plan: int = 0):
+            plan: int = 0, bound: int = 0):
     """frames: [B][H][W] uint16/uint8/float32 -> (lists per frame per column, costs [B][n_cols],
     counts [B][n_cols], handle).  plan: DP launch plan (0 auto, 4 or 8 warps per column;
-    a forced plan is checked against the launch the library reports)."""
+    a forced plan is checked against the launch the library reports; bound: the int32
+    kernel's chunk bound, 0 auto, 1 off, 2 on)."""
     import torch
     from paper_1610_04124_b200 import stixels as S
     B, H, W = frames.shape
@@ -23,6 +24,8 @@ def run_gpu(p: dict, frames: np.ndarray, max_batch: int | None = None, host: boo
     hd = S.Handle(params, W, H, max_batch or B)
     if plan:
         hd.set_launch_plan(plan)
+    if bound:
+        hd.set_chunk_bound(bound)
     if host:
         out = np.zeros((B, hd.n_cols, hd.cap, 12), np.uint8)
         cnt = np.zeros((B, hd.n_cols), np.int32)

@@ -232,6 +232,45 @@ def test_chunk_bound_skips_and_stays_exact():
     _assert_exact(mp.make(ground_slope=0.3), fr)
 
 
+@pytest.mark.parametrize("H,W", [(440, 1024), (160, 400), (96, 300)])
+def test_chunk_bound_on_off_identical(H, W):
+    """stixels_set_chunk_bound: the int32 kernel with the chunk bound forced on and
+    forced off gives byte-identical lists and costs, under both launch plans, and
+    both equal the oracle's; the bound is forced on also below its automatic
+    threshold (320 rows), where it is off by default, so short columns with few
+    chunks exercise it as well."""
+    frames = _frames_c2(2, seed0=3400 + H, W=W, H=H)
+    p = mp.make()
+    o, oc = run_oracle(p, frames)
+    for plan in (4, 8):
+        res = {}
+        for bound in (1, 2):
+            g, gc, cnt, hd = run_gpu(p, frames, plan=plan, bound=bound)
+            bad = compare_exact(g, gc, o, oc, p["cost_frac_bits"])
+            assert not bad, f"plan {plan} bound {bound}: {len(bad)} mismatching columns, first: {bad[:2]}"
+            res[bound] = (g, gc.tobytes(), hd.skipped_cells())
+        assert res[1][0] == res[2][0] and res[1][1] == res[2][1]
+        assert res[1][2] == 0                            # off: nothing skipped
+
+
+def test_chunk_bound_mode_errors():
+    """stixels_set_chunk_bound rejects modes outside 0..2, and forcing it on for a
+    model without the int32 kernel (continuous mode) is UNSUPPORTED."""
+    from paper_1610_04124_b200 import stixels as S
+    H, W = 440, 200
+    hd = S.Handle(S.params_from_dict(mp.make(), H), W, H, 1)
+    with pytest.raises(Exception):
+        hd.set_chunk_bound(3)
+    hd.set_chunk_bound(2)
+    hd.set_chunk_bound(0)
+    hd.destroy()
+    hc = S.Handle(S.params_from_dict(mp.make(cost_frac_bits=0), H), W, H, 1)
+    with pytest.raises(Exception):
+        hc.set_chunk_bound(2)
+    hc.set_chunk_bound(1)
+    hc.destroy()
+
+
 def test_dp_variants_exact():
     """Each DP kernel variant stixels_create picks is exact against
     the oracle: the int32 atomic-band path (band <= 3, the default model), the
