@@ -211,6 +211,21 @@ def test_c2_frames_exact():
     assert hd.last_launch_count() == 2      # reduce_kernel + dp_kernel
 
 
+def test_full_batch_path_exact_sampled():
+    """The headline path at a batch large enough for the strip reduction (48 frames
+    of 1024x440: 672 strips of 32 rows >= 4 per SM) and the int32 kernel with the
+    chunk bound, through stixels_compute: every column of 6 sampled frames equals
+    the oracle exactly."""
+    frames = _frames_c2(48, seed0=3500)
+    p = mp.make()
+    g, gc, cnt, hd = run_gpu(p, frames)
+    assert hd.skipped_cells() > 0
+    pick = [0, 9, 17, 30, 41, 47]
+    o, oc = run_oracle(p, frames[pick])
+    bad = compare_exact([g[i] for i in pick], gc[pick], o, oc, p["cost_frac_bits"])
+    assert not bad, f"{len(bad)} mismatching columns, first: {bad[:2]}"
+
+
 def test_chunk_bound_skips_and_stays_exact():
     """The int32 kernel's exact chunk bound (columns of >= 320 rows): on C2 frames
     it skips a substantial share of the rectangle cells (stixels_skipped_cells) and
