@@ -641,6 +641,31 @@ def test_reduce_strip_kernel_bit_exact(fmt, s, pad):
             hd.destroy()
 
 
+def test_reduce_strip_kernel_short_frames():
+    """The strip reduction on frames shorter than one strip (20 rows: every strip
+    is a ragged one) over 640 frames, u16 with an even number of 16-byte units per
+    row (the shared-memory row stride then gets its 16-byte pad): bit-exact."""
+    import torch
+    from oracle import oracle as orc
+    from paper_1610_04124_b200 import stixels as S
+    H, D, B, s = 20, 64, 640, 5
+    W = 160                                            # 320 bytes = 20 units of 16
+    rng = np.random.default_rng(4242)
+    full = rng.integers(0, (D + 2) * 16, size=(B, H, W)).astype(np.uint16)
+    full[rng.random(full.shape) < 0.1] = 0xFFFF
+    p = mp.make(max_disparity=D, stixel_width=s, invalid_value=0xFFFF, disp_frac_bits=4)
+    hd = S.Handle(S.params_from_dict(p, H), W, H, B)
+    cols = torch.empty((B, hd.n_cols, H), dtype=torch.int16, device="cuda")
+    hd.reduce(torch.from_numpy(full.view(np.int16)).cuda(), cols, row_pitch_bytes=W * 2)
+    hd.sync()
+    got = cols.cpu().numpy().view(np.uint16).astype(np.int32)
+    got[got == 0xFFFF] = -1
+    for b in range(0, B, 37):
+        want = orc.reduce(full[b], s, 4, 0xFFFF, D)
+        assert (got[b] == want).all(), (b, np.argwhere(got[b] != want)[:3])
+    hd.destroy()
+
+
 @pytest.mark.parametrize("D,q", [(64, 4), (256, 8)])
 def test_top_of_range_pixels_exact(D, q):
     """L#27: pixels in [D - 1/2, D) keep their value for the ground and sky terms
