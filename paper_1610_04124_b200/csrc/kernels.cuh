@@ -966,7 +966,7 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
   // IADD3 and no conversion; otherwise fp32.
   using CT = std::conditional_t<IW, int, float>;
 
-  constexpr int kRectUnroll = IW ? (DP == 128 ? 4 : 2) : 1;
+  constexpr int kRectUnroll = IW ? 2 : 1;
   struct Acc { CT b0, b1; int a0, a1; };              // running minima {cost, argj} of t0 / t1
   const int hw = lane >> 4;
   const uint32_t rec_s = (uint32_t)__cvta_generic_to_shared(cs.rec);
@@ -1056,8 +1056,9 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
     int f0 = fmean(r, tg.T0, tg.N0), f1 = fmean(r, tg.T1, tg.N1);
     __syncwarp();
     // bottoms per iteration (A/B on the B200): fp32 path 4 (unroll 2: -3.5%, 8: -13%);
-    // IW int32 path, DP = 128: 16 (unroll 1: -0.5%, 2: -2.1%, 8: -7%); DP = 256: 8
-    // (unroll 4: -2%)
+    // IW int32 path 8 (with the chunk bound, where the kernel's size decides its
+    // instruction-cache misses: 16 bottoms -1.4% at 1024x440 and -3.4% at 1024x220,
+    // 4 bottoms -1.8%; before the bound 16 had been best at DP = 128)
 #pragma unroll kRectUnroll
     for (int jj = 0; jj < nsteps; jj += 4) {
 #pragma unroll
