@@ -1432,6 +1432,8 @@ __global__ void __launch_bounds__(32 * kCW * 4, 1) dp_kernel(const __grid_consta
         const int* pv = reinterpret_cast<const int*>(cs.priv);
         int4* cl = reinterpret_cast<int4*>(cells_of(bt));
         const int wq = t0 >> 5, nq = nthr >> 5;       // this warp's index among nq warps
+        // (not unrolled: the smaller kernel has fewer instruction-cache misses, +1.5%)
+#pragma unroll 1
         for (int it = wq; it < 16; it += nq) {
           const bool lo = lane < 31 - it;
           const int jr = lo ? it : 30 - it;
